@@ -1,0 +1,232 @@
+/* perfseer_b200.h — the drop-in C ABI of the B200 measured-kernel and
+ * calibration path.
+ *
+ * The reference exposes this path as C++ virtuals and free functions; this
+ * header is what a binding (cgo / JNI / ctypes / plain C++) links against.
+ * Every entry point returns int status (0 = OK); on failure the message is
+ * available from ps_last_error() (thread-local, valid until the next call on
+ * the same thread). No torch or C++ types cross this boundary.
+ *
+ * Reference interfaces replaced (paths relative to the reference's proj/):
+ *   ps_init / ps_destroy / ps_measure
+ *       perfseer::Executor::id/measure        include/perfseer/executor.hpp:16-23
+ *       (the GPU executor the reference leaves as an extension point)
+ *   ps_measure_summary
+ *       perfseer::measure_kernel + summarize  src/executor.cpp:14-48
+ *   ps_desc_from_id
+ *       variant_id() parsing (the executor dispatches on Kernel::name, which is
+ *       the generator variant id)             src/uipick.cpp:149-154,197-198
+ *   ps_run_verify
+ *       parity hook: runs one generated kernel on caller-owned HOST buffers
+ *       (the reference's own interpreter is tests/support.hpp:50-162)
+ *   ps_fit_lm_batched
+ *       perfseer::fit_model (Levenberg-Marquardt) src/model.cpp:485-606
+ *   ps_eval_batched
+ *       perfseer::predict + report ranking     src/model.cpp:615-623,
+ *                                              tools/perfseer.cpp:452-469
+ *
+ * Threading: one ps_ctx per GPU; a ps_ctx must not be used concurrently
+ * (executors are exclusive resources, executor.hpp:13-15).
+ * Different contexts may be driven from different host threads.
+ */
+#ifndef PERFSEER_B200_H_
+#define PERFSEER_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PS_OK 0
+#define PS_ERR_ARG 1      /* bad argument / unknown generator (SemanticError-like) */
+#define PS_ERR_CUDA 2     /* CUDA runtime failure (mapped to EvalError by CudaExecutor) */
+#define PS_ERR_NOMEM 3    /* device allocation failed */
+#define PS_ERR_STATE 4    /* call out of order */
+
+typedef struct ps_ctx ps_ctx;
+
+/* Generators: one per UIPiCK builder (src/uipick.cpp:295-664) plus the DG
+ * application variants designed from PAPER.md:2341-2442. */
+enum ps_generator {
+  PS_GEN_GMEM_PATTERN = 1,   /* make_gmem_pattern      uipick.cpp:295-315 */
+  PS_GEN_FLOPS = 2,          /* make_flops_pattern     uipick.cpp:317-378 */
+  PS_GEN_LMEM_SHUFFLE = 3,   /* make_lmem_shuffle      uipick.cpp:380-404 */
+  PS_GEN_BARRIER = 4,        /* make_barrier_knl       uipick.cpp:406-423 */
+  PS_GEN_EMPTY = 5,          /* make_empty_knl         uipick.cpp:425-432 */
+  PS_GEN_OVERLAP = 6,        /* make_overlap_knl       uipick.cpp:434-462 */
+  PS_GEN_MATMUL = 7,         /* make_matmul_sq         uipick.cpp:464-554 */
+  PS_GEN_MATMUL_RM = 8,      /* make_matmul_sq_rm      uipick.cpp:556-581 */
+  PS_GEN_FD = 9,             /* make_fd_stencil        uipick.cpp:583-639 */
+  PS_GEN_FD_RM = 10,         /* make_fd_stencil_rm     uipick.cpp:641-664 */
+  PS_GEN_DG = 11,            /* DG differentiation */
+  PS_GEN_DG_RM = 12,         /* DG work-removed */
+  PS_GEN_MATMUL_TC = 13      /* extra: tcgen05 dense contraction (not a paper variant) */
+};
+
+enum ps_dtype { PS_F32 = 0, PS_F64 = 1 };
+enum ps_flop_op { PS_OP_ADD = 0, PS_OP_MUL = 1, PS_OP_MADD = 2 };
+/* keep argument of the *_rm generators */
+enum ps_keep { PS_KEEP_NONE = 0, PS_KEEP_A = 1, PS_KEEP_B = 2, PS_KEEP_U = 3, PS_KEEP_RES = 4,
+               PS_KEEP_DM = 5 };
+/* DG variants */
+enum ps_dg_variant { PS_DG_NOPF = 0, PS_DG_UPF = 1, PS_DG_DMPF = 2, PS_DG_DMPF_T = 3 };
+/* input fill modes */
+enum ps_fill { PS_FILL_SEED17 = 0, PS_FILL_UNIFORM = 1 };
+
+/* Plain-old-data description of one generated measurement kernel, parsed
+ * from its variant id ("gen__arg-value__..."). Unused fields are 0. */
+typedef struct ps_kernel_desc {
+  int32_t gen;          /* enum ps_generator */
+  int32_t dtype;        /* enum ps_dtype */
+  int32_t op;           /* flops: enum ps_flop_op */
+  int32_t keep;         /* *_rm: enum ps_keep */
+  int64_t nelements;    /* pattern generators: E */
+  int64_t lsize0, lsize1;
+  int64_t lid_stride0, lid_stride1;
+  int64_t n_inputs;     /* gmem_pattern: n_input_arrays */
+  int64_t m;            /* flops/lmem/barrier/overlap iteration count */
+  int64_t num_groups;   /* empty_knl */
+  int64_t n;            /* matmul / finite_diff size */
+  int32_t prefetch;     /* matmul: 1 = PF, 0 = noPF */
+  int32_t tile;         /* finite_diff: 16 or 18 */
+  int64_t nel;          /* DG: number of elements */
+  int64_t np;           /* DG: padded nodes per element (multiple of 16) */
+  int64_t nmat;         /* DG: number of derivative matrices (3) */
+  int32_t dg_variant;   /* enum ps_dg_variant */
+  int32_t reserved;
+} ps_kernel_desc;
+
+/* Buffer layout of a kernel's global arrays (host side, no GPU needed). */
+#define PS_MAX_ARRAYS 4
+typedef struct ps_io_info {
+  int32_t n_inputs;
+  int32_t n_outputs;
+  int32_t elem_bytes;
+  int32_t reserved;
+  int64_t input_elems[PS_MAX_ARRAYS];
+  int64_t output_elems[PS_MAX_ARRAYS];
+  /* algorithmic work per launch, for roofline reporting */
+  double bytes_global;   /* compulsory DRAM bytes (each array touched once) */
+  double flops;          /* floating-point operations (madd = 2) */
+  double bytes_shared;   /* shared-memory bytes moved */
+} ps_io_info;
+
+const char* ps_last_error(void);
+const char* ps_version(void);
+
+/* --- host-only helpers (no GPU required) -------------------------------- */
+int ps_desc_from_id(const char* variant_id, ps_kernel_desc* out);
+int ps_kernel_io(const ps_kernel_desc* desc, ps_io_info* out);
+
+/* --- device context ------------------------------------------------------ */
+int ps_init(int device, ps_ctx** out);
+int ps_destroy(ps_ctx* ctx);
+int ps_device_info(ps_ctx* ctx, int* sm_count, int* sm_clock_khz, size_t* l2_bytes,
+                   size_t* free_bytes);
+
+/* Allocates (grow-only, cached) device buffers for desc and fills inputs on
+ * the device with the deterministic pattern (PS_FILL_SEED17: the reference
+ * test fixture's 1 + FNV1a(array, flat) % 17, tests/support.hpp:35-44;
+ * PS_FILL_UNIFORM: U[-1,1) from `seed`). */
+int ps_prepare(ps_ctx* ctx, const ps_kernel_desc* desc, int fill_mode, uint64_t seed);
+
+/* Executor::measure: `warmup` untimed launches then `trials` launches each
+ * bracketed by CUDA events on the context stream; per-trial seconds into the
+ * caller-owned out_seconds[trials]. Prepares buffers on first use. */
+int ps_measure(ps_ctx* ctx, const ps_kernel_desc* desc, int warmup, int trials,
+               double* out_seconds);
+
+/* measure_kernel + summarize (drop trials > filter_factor * median, mean of
+ * survivors, src/executor.cpp:14-38). */
+int ps_measure_summary(ps_ctx* ctx, const ps_kernel_desc* desc, int warmup, int trials,
+                       double filter_factor, double* mean_seconds, int* kept_trials);
+
+/* Launch `launches` back-to-back kernels on prepared buffers and return the
+ * total device time (CUDA events) — used by the bench's timed region. */
+int ps_run_timed(ps_ctx* ctx, const ps_kernel_desc* desc, int launches, double* seconds);
+
+/* Parity hook: host inputs -> device, one launch, device -> host outputs.
+ * inputs[i] has input_elems[i] elements of the kernel dtype; outputs are
+ * zero-initialised on the device before the launch. */
+int ps_run_verify(ps_ctx* ctx, const ps_kernel_desc* desc, const void* const* inputs,
+                  int n_inputs, void* const* outputs, int n_outputs);
+
+/* Device pointer of the prepared input/output i (for zero-copy callers). */
+int ps_buffer(ps_ctx* ctx, int is_output, int index, void** dev_ptr, int64_t* elems);
+
+/* --- calibration (K17) and prediction (K18) ------------------------------ */
+
+/* Compiled model expression: postfix bytecode over params/features/constants
+ * (compiled host-side from the reference model grammar, model.cpp:50-234). */
+#define PS_BC_NUM 0     /* push consts[arg]            */
+#define PS_BC_PARAM 1   /* push params[arg]            */
+#define PS_BC_FEAT 2    /* push features[arg]          */
+#define PS_BC_ADD 3
+#define PS_BC_SUB 4
+#define PS_BC_MUL 5
+#define PS_BC_DIV 6
+#define PS_BC_TANH 7
+typedef struct ps_bytecode {
+  int32_t n_ops;
+  int32_t n_consts;
+  const int32_t* ops;     /* [n_ops] opcode << 16 | arg */
+  const double* consts;   /* [n_consts] */
+} ps_bytecode;
+
+typedef struct ps_fit_opts {
+  double lambda0, lambda_decrease, lambda_increase, step_tol, grad_tol;
+  int32_t max_iterations;
+  int32_t nonnegative;
+} ps_fit_opts;
+
+typedef struct ps_fit_stats {
+  double residual_norm;
+  int32_t iterations;
+  int32_t converged;
+  int32_t status;        /* 0 ok, 1 damping overflow (divergence) */
+  int32_t reserved;
+} ps_fit_stats;
+
+/* Batched LM: `nbatch` independent fits of one model (np params, nf
+ * features) over nr rows each. features: [nbatch][nr][nf], t: [nbatch][nr],
+ * params_inout: [nbatch][np] (initial point in, fitted out), stats[nbatch].
+ * jac holds np bytecodes (dg/dp_i). Host buffers. */
+int ps_fit_lm_batched(ps_ctx* ctx, const ps_bytecode* model, const ps_bytecode* jac, int np,
+                      int nf, const double* features, const double* t, int nr, int nbatch,
+                      const ps_fit_opts* opts, double* params_inout, ps_fit_stats* stats);
+
+/* Batched prediction over a variant space. Each of the nvar variants carries
+ * a count table: nf features, each an exact polynomial in the point's
+ * parameters with a rational scale (feature = poly(point) / den), see
+ * DESIGN.md "K18". points: [npts][nparams] int64; params_fit: [nvar][np];
+ * pred: [npts][nvar] seconds; argmin: [npts][ngroups] winning variant index
+ * per application group (strict '<' first minimum, tools/perfseer.cpp:458-467). */
+typedef struct ps_variant_tables {
+  int32_t nvar;          /* variants */
+  int32_t nf;            /* features per variant (model feature order) */
+  int32_t nparams;       /* point coordinates */
+  int32_t max_terms;     /* terms per feature polynomial */
+  int32_t ngroups;       /* application groups for argmin */
+  int32_t reserved;
+  const int32_t* var_group;     /* [nvar] group index */
+  const int32_t* var_model;     /* [nvar] model index into models[] */
+  const int32_t* var_coord;     /* [nvar][4] which point coordinate feeds symbol 0..3 (-1 unused) */
+  const int64_t* coef_num;      /* [nvar][nf][max_terms] */
+  const int64_t* coef_den;      /* [nvar][nf] common denominator (already includes granularity) */
+  const int8_t* exps;           /* [nvar][nf][max_terms][4] exponents of symbols 0..3 */
+  int32_t nmodels;
+  int32_t model_np;             /* parameters per model (max) */
+  const ps_bytecode* models;    /* [nmodels] */
+  const double* params;         /* [nmodels][model_np] */
+} ps_variant_tables;
+
+int ps_eval_batched(ps_ctx* ctx, const ps_variant_tables* tables, const int64_t* points,
+                    int64_t npts, double* pred, uint8_t* argmin);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PERFSEER_B200_H_ */

@@ -1,0 +1,155 @@
+// K14/K15: DG element-wise differentiation, res[m,k,i] = sum_j dm[m,i,j] u[k,j]
+// (the reference ships no DG generator, SPEC.md:16,536 —
+// the IR these kernels realise is defined by this repo's dg_diff builder,
+// DESIGN.md "DG variants").
+//
+// Common geometry: i split by 16 (g.1/l.1), k split by 16 (g.0/l.0); a
+// work-item owns (k, i) and loops over m and j. Layouts (row-major):
+//   dm  [nmat][Np][Np]
+//   u   [nel][Np]         (dmPFtrans: [Np][nel], k fastest)
+//   res [nmat][nel][Np]   (dmPFtrans: [nmat][Np][nel], k fastest)
+// Accumulation order per (m, k, i): j ascending from 0, fused multiply-add,
+// identical in all four variants (so all four produce the same bits).
+#pragma once
+
+#include "device_common.cuh"
+
+namespace ps {
+
+struct DgDims {
+  int64_t nel;
+  int np;
+  int nmat;
+};
+
+__device__ __forceinline__ int64_t dg_u_idx(bool trans, const DgDims& d, int64_t k, int j) {
+  return trans ? (int64_t)j * d.nel + k : k * d.np + j;
+}
+__device__ __forceinline__ int64_t dg_res_idx(bool trans, const DgDims& d, int m, int64_t k,
+                                              int i) {
+  return trans ? ((int64_t)m * d.np + i) * d.nel + k : ((int64_t)m * d.nel + k) * d.np + i;
+}
+
+// noPF: no local memory; m outermost, reduction over j.
+__global__ void __launch_bounds__(256) dg_nopf(const float* __restrict__ dm,
+                                               const float* __restrict__ u,
+                                               float* __restrict__ res, DgDims d) {
+  const int64_t k = (int64_t)blockIdx.x * 16 + threadIdx.x;
+  const int i = blockIdx.y * 16 + threadIdx.y;
+  for (int m = 0; m < d.nmat; ++m) {
+    const float* dmrow = dm + ((int64_t)m * d.np + i) * d.np;
+    const float* urow = u + k * d.np;
+    float acc = 0.f;
+#pragma unroll 8
+    for (int j = 0; j < d.np; ++j) acc = __fmaf_rn(dmrow[j], urow[j], acc);
+    res[dg_res_idx(false, d, m, k, i)] = acc;
+  }
+}
+
+// uPF: 16x16 tiles of u staged in shared memory per j_out (two barriers per
+// tile), m privatised into NMAT accumulators, loop order j_out, j_in, m.
+template <int NMAT>
+__global__ void __launch_bounds__(256) dg_upf(const float* __restrict__ dm,
+                                              const float* __restrict__ u,
+                                              float* __restrict__ res, DgDims d) {
+  __shared__ float uf[16][17];
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int64_t k0 = (int64_t)blockIdx.x * 16;
+  const int i = blockIdx.y * 16 + ly;
+  float acc[NMAT];
+#pragma unroll
+  for (int m = 0; m < NMAT; ++m) acc[m] = 0.f;
+  for (int jo = 0; jo < d.np / 16; ++jo) {
+    bar_sync();
+    uf[ly][lx] = u[(k0 + ly) * d.np + jo * 16 + lx];  // u_fetch[k_in, j_in], j_in -> l.0
+    bar_sync();
+#pragma unroll
+    for (int ji = 0; ji < 16; ++ji) {
+      const float uv = uf[lx][ji];
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m)
+        acc[m] = __fmaf_rn(dm[((int64_t)m * d.np + i) * d.np + jo * 16 + ji], uv, acc[m]);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < NMAT; ++m) res[dg_res_idx(false, d, m, k0 + lx, i)] = acc[m];
+}
+
+// dmPF / dmPFtrans: per m and j_out, a 16x16 tile of dm staged in shared
+// memory (two barriers per tile); u read directly (strided by Np in dmPF,
+// unit-stride across lid(0) in the transposed layout).
+template <bool TRANS>
+__global__ void __launch_bounds__(256) dg_dmpf(const float* __restrict__ dm,
+                                               const float* __restrict__ u,
+                                               float* __restrict__ res, DgDims d) {
+  __shared__ float dmf[16][17];
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int64_t k = (int64_t)blockIdx.x * 16 + lx;
+  const int i0 = blockIdx.y * 16;
+  for (int m = 0; m < d.nmat; ++m) {
+    float acc = 0.f;
+    for (int jo = 0; jo < d.np / 16; ++jo) {
+      bar_sync();
+      dmf[ly][lx] = dm[((int64_t)m * d.np + i0 + ly) * d.np + jo * 16 + lx];
+      bar_sync();
+#pragma unroll
+      for (int ji = 0; ji < 16; ++ji)
+        acc = __fmaf_rn(dmf[ly][ji], u[dg_u_idx(TRANS, d, k, jo * 16 + ji)], acc);
+    }
+    res[dg_res_idx(TRANS, d, m, k, i0 + ly)] = acc;
+  }
+}
+
+// Work-removed DG (remove_work semantics, transforms.cpp:317-514): the kept
+// global load accumulates into tgt_read in the variant's statement order; a
+// kept res store writes tgt_read (= 0); otherwise tgt_read_dest[i, k] (lid(0)
+// fastest) receives tgt_read.
+// keep: 3 = u, 5 = dm, 4 = res.  variant: 0 noPF, 1 uPF, 2 dmPF, 3 dmPFtrans.
+template <int VARIANT, int KEEP>
+__global__ void __launch_bounds__(256) dg_rm(const float* __restrict__ src,
+                                             float* __restrict__ dst, DgDims d) {
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int64_t k0 = (int64_t)blockIdx.x * 16;
+  const int64_t k = k0 + lx;
+  const int i0 = blockIdx.y * 16;
+  const int i = i0 + ly;
+  constexpr bool TRANS = VARIANT == 3;
+  if constexpr (KEEP == 4) {
+    for (int m = 0; m < d.nmat; ++m) dst[dg_res_idx(TRANS, d, m, k, i)] = 0.f;
+    return;
+  } else {
+    float acc = 0.f;
+    const int njo = d.np / 16;
+    if constexpr (VARIANT == 0) {
+      // statement within (m, k, i), reduction j
+      for (int m = 0; m < d.nmat; ++m)
+        for (int j = 0; j < d.np; ++j)
+          acc = __fadd_rn(acc, KEEP == 3 ? src[k * d.np + j]
+                                         : src[((int64_t)m * d.np + i) * d.np + j]);
+    } else if constexpr (VARIANT == 1) {
+      if constexpr (KEEP == 3) {
+        // fetch: one u load per (work-item, j_out)
+        for (int jo = 0; jo < njo; ++jo) acc = __fadd_rn(acc, src[(k0 + ly) * d.np + jo * 16 + lx]);
+      } else {
+        for (int jo = 0; jo < njo; ++jo)
+          for (int ji = 0; ji < 16; ++ji)
+            for (int m = 0; m < d.nmat; ++m)
+              acc = __fadd_rn(acc, src[((int64_t)m * d.np + i) * d.np + jo * 16 + ji]);
+      }
+    } else {
+      if constexpr (KEEP == 3) {
+        for (int m = 0; m < d.nmat; ++m)
+          for (int jo = 0; jo < njo; ++jo)
+            for (int ji = 0; ji < 16; ++ji)
+              acc = __fadd_rn(acc, src[dg_u_idx(TRANS, d, k, jo * 16 + ji)]);
+      } else {
+        for (int m = 0; m < d.nmat; ++m)
+          for (int jo = 0; jo < njo; ++jo)
+            acc = __fadd_rn(acc, src[((int64_t)m * d.np + i0 + ly) * d.np + jo * 16 + lx]);
+      }
+    }
+    dst[(int64_t)i * d.nel + k] = acc;
+  }
+}
+
+}  // namespace ps

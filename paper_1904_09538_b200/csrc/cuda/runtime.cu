@@ -1,0 +1,842 @@
+// C-ABI implementation of the measurement executor (include/perfseer_b200.h).
+//
+// This is the B200 side of perfseer::Executor (reference
+// include/perfseer/executor.hpp:16-23): a context owns one CUDA stream, a
+// pool of CUDA events and grow-only device buffers; ps_measure times each
+// trial with a pair of events on that stream (the reference's contract is
+// per-trial seconds, SPEC.md:547-549, 60 trials by default).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../../include/perfseer_b200.h"
+#include "suite_kernels.cuh"
+#include "runtime_internal.h"
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+namespace ps {
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define PS_CUDA(call)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return set_error(PS_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                       __FILE__, __LINE__);                                                 \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Variant-id parsing: "gen__key-value__key-value" with keys sorted
+// (variant_id, uipick.cpp:149-154).
+
+static bool to_i64(const std::string& s, int64_t* out) {
+  if (s.empty()) return false;
+  char* end = nullptr;
+  long long v = strtoll(s.c_str(), &end, 10);
+  if (*end != '\0') return false;
+  *out = v;
+  return true;
+}
+
+static bool to_bool(const std::string& s, int32_t* out) {
+  if (s == "True" || s == "true" || s == "1") return (*out = 1), true;
+  if (s == "False" || s == "false" || s == "0") return (*out = 0), true;
+  return false;
+}
+
+int parse_variant_id(const char* id, ps_kernel_desc* d) {
+  if (!id || !d) return set_error(PS_ERR_ARG, "ps_desc_from_id: null argument");
+  std::memset(d, 0, sizeof *d);
+  std::string s(id);
+  std::vector<std::string> parts;
+  size_t pos = 0;
+  while (true) {
+    size_t next = s.find("__", pos);
+    parts.push_back(s.substr(pos, next == std::string::npos ? std::string::npos : next - pos));
+    if (next == std::string::npos) break;
+    pos = next + 2;
+  }
+  const std::string gen = parts[0];
+  std::map<std::string, std::string> args;
+  for (size_t i = 1; i < parts.size(); ++i) {
+    size_t dash = parts[i].find('-');
+    if (dash == std::string::npos)
+      return set_error(PS_ERR_ARG, "malformed variant argument '%s' in '%s'", parts[i].c_str(), id);
+    args[parts[i].substr(0, dash)] = parts[i].substr(dash + 1);
+  }
+  auto need_i = [&](const char* key, int64_t* out) -> bool {
+    auto it = args.find(key);
+    if (it == args.end() || !to_i64(it->second, out)) {
+      set_error(PS_ERR_ARG, "variant '%s' lacks integer argument '%s'", id, key);
+      return false;
+    }
+    return true;
+  };
+  auto dtype_of = [&]() -> bool {
+    auto it = args.find("dtype");
+    if (it == args.end()) {
+      d->dtype = PS_F32;
+      return true;
+    }
+    if (it->second == "float32") return (d->dtype = PS_F32), true;
+    if (it->second == "float64") return (d->dtype = PS_F64), true;
+    set_error(PS_ERR_ARG, "variant '%s': unsupported dtype '%s'", id, it->second.c_str());
+    return false;
+  };
+  auto pattern = [&]() -> bool {
+    return need_i("nelements", &d->nelements) && need_i("lsize_0", &d->lsize0) &&
+           need_i("lsize_1", &d->lsize1) && need_i("lid_stride_0", &d->lid_stride0) &&
+           need_i("lid_stride_1", &d->lid_stride1);
+  };
+
+  if (!dtype_of()) return PS_ERR_ARG;
+  bool ok = true;
+  if (gen == "gmem_pattern") {
+    d->gen = PS_GEN_GMEM_PATTERN;
+    ok = pattern() && need_i("n_input_arrays", &d->n_inputs);
+  } else if (gen == "flops_add_pattern" || gen == "flops_mul_pattern" ||
+             gen == "flops_madd_pattern") {
+    d->gen = PS_GEN_FLOPS;
+    d->op = gen == "flops_add_pattern" ? PS_OP_ADD
+            : gen == "flops_mul_pattern" ? PS_OP_MUL
+                                         : PS_OP_MADD;
+    ok = pattern() && need_i("m", &d->m);
+  } else if (gen == "lmem_shuffle") {
+    d->gen = PS_GEN_LMEM_SHUFFLE;
+    ok = pattern() && need_i("m", &d->m);
+  } else if (gen == "barrier_knl") {
+    d->gen = PS_GEN_BARRIER;
+    ok = pattern() && need_i("m", &d->m);
+  } else if (gen == "empty_knl") {
+    d->gen = PS_GEN_EMPTY;
+    ok = need_i("num_groups", &d->num_groups);
+  } else if (gen == "overlap_knl") {
+    d->gen = PS_GEN_OVERLAP;
+    ok = pattern() && need_i("m", &d->m);
+  } else if (gen == "matmul_sq" || gen == "matmul_sq_rm" || gen == "matmul_sq_tc") {
+    d->gen = gen == "matmul_sq" ? PS_GEN_MATMUL
+             : gen == "matmul_sq_rm" ? PS_GEN_MATMUL_RM
+                                     : PS_GEN_MATMUL_TC;
+    ok = need_i("n", &d->n) && need_i("lsize_0", &d->lsize0) && need_i("lsize_1", &d->lsize1);
+    if (ok && d->gen != PS_GEN_MATMUL_TC) {
+      auto it = args.find("prefetch");
+      if (it == args.end() || !to_bool(it->second, &d->prefetch))
+        return set_error(PS_ERR_ARG, "variant '%s' lacks boolean 'prefetch'", id);
+    }
+    if (ok && d->gen == PS_GEN_MATMUL_RM) {
+      auto it = args.find("keep");
+      if (it == args.end() || (it->second != "a" && it->second != "b"))
+        return set_error(PS_ERR_ARG, "variant '%s': keep must be a or b", id);
+      d->keep = it->second == "a" ? PS_KEEP_A : PS_KEEP_B;
+    }
+  } else if (gen == "finite_diff" || gen == "finite_diff_rm") {
+    d->gen = gen == "finite_diff" ? PS_GEN_FD : PS_GEN_FD_RM;
+    ok = need_i("n", &d->n);
+    auto it = args.find("tile");
+    if (ok) {
+      if (it == args.end() || (it->second != "16x16" && it->second != "18x18"))
+        return set_error(PS_ERR_ARG, "variant '%s': tile must be 16x16 or 18x18", id);
+      d->tile = it->second == "16x16" ? 16 : 18;
+    }
+    if (ok && d->gen == PS_GEN_FD_RM) {
+      auto kt = args.find("keep");
+      if (kt == args.end() || (kt->second != "u" && kt->second != "res"))
+        return set_error(PS_ERR_ARG, "variant '%s': keep must be u or res", id);
+      d->keep = kt->second == "u" ? PS_KEEP_U : PS_KEEP_RES;
+    }
+  } else if (gen == "dg_diff" || gen == "dg_diff_rm") {
+    d->gen = gen == "dg_diff" ? PS_GEN_DG : PS_GEN_DG_RM;
+    ok = need_i("nelements", &d->nel) && need_i("nunit_nodes", &d->np) &&
+         need_i("nmatrices", &d->nmat);
+    auto it = args.find("variant");
+    if (ok) {
+      if (it == args.end()) return set_error(PS_ERR_ARG, "variant '%s' lacks 'variant'", id);
+      if (it->second == "noPF") d->dg_variant = PS_DG_NOPF;
+      else if (it->second == "uPF") d->dg_variant = PS_DG_UPF;
+      else if (it->second == "dmPF") d->dg_variant = PS_DG_DMPF;
+      else if (it->second == "dmPFtrans") d->dg_variant = PS_DG_DMPF_T;
+      else return set_error(PS_ERR_ARG, "variant '%s': unknown DG variant", id);
+    }
+    if (ok && d->gen == PS_GEN_DG_RM) {
+      auto kt = args.find("keep");
+      if (kt == args.end()) return set_error(PS_ERR_ARG, "variant '%s' lacks 'keep'", id);
+      if (kt->second == "u") d->keep = PS_KEEP_U;
+      else if (kt->second == "dm") d->keep = PS_KEEP_DM;
+      else if (kt->second == "res") d->keep = PS_KEEP_RES;
+      else return set_error(PS_ERR_ARG, "variant '%s': keep must be u, dm or res", id);
+    }
+  } else {
+    return set_error(PS_ERR_ARG, "unknown generator '%s' in variant id '%s'", gen.c_str(), id);
+  }
+  if (!ok) return PS_ERR_ARG;
+  return validate_desc(d);
+}
+
+int validate_desc(const ps_kernel_desc* d) {
+  auto pattern_ok = [&]() -> int {
+    if (d->nelements < 1 || d->lsize0 < 1 || d->lsize1 < 1 || d->lid_stride0 < 1 ||
+        d->lid_stride1 < 1)
+      return set_error(PS_ERR_ARG, "pattern layout arguments must be positive");
+    if (d->lsize0 * d->lsize1 > 1024)
+      return set_error(PS_ERR_ARG, "work-group size %lld exceeds 1024 threads",
+                       (long long)(d->lsize0 * d->lsize1));
+    if (d->lid_stride1 % (d->lid_stride0 * d->lsize0) != 0)
+      return set_error(PS_ERR_ARG, "lid_stride_1 must be a multiple of lid_stride_0*lsize_0");
+    if (d->nelements % (d->lid_stride1 * d->lsize1) != 0)
+      return set_error(PS_ERR_ARG, "nelements must be a multiple of lid_stride_1*lsize_1");
+    return PS_OK;
+  };
+  switch (d->gen) {
+    case PS_GEN_GMEM_PATTERN:
+      if (d->n_inputs != 1 && d->n_inputs != 2)
+        return set_error(PS_ERR_ARG, "gmem_pattern supports 1 or 2 input arrays");
+      return pattern_ok();
+    case PS_GEN_FLOPS:
+      if (d->dtype != PS_F32) return set_error(PS_ERR_ARG, "flops kernels are float32");
+      if (d->m < 1) return set_error(PS_ERR_ARG, "flops iteration count must be >= 1");
+      return pattern_ok();
+    case PS_GEN_LMEM_SHUFFLE:
+    case PS_GEN_BARRIER:
+    case PS_GEN_OVERLAP:
+      if (d->dtype != PS_F32) return set_error(PS_ERR_ARG, "pattern kernel is float32 only");
+      if (d->m < 0) return set_error(PS_ERR_ARG, "iteration count must be >= 0");
+      return pattern_ok();
+    case PS_GEN_EMPTY:
+      if (d->num_groups < 1) return set_error(PS_ERR_ARG, "num_groups must be >= 1");
+      return PS_OK;
+    case PS_GEN_MATMUL:
+    case PS_GEN_MATMUL_RM:
+    case PS_GEN_MATMUL_TC:
+      if (d->lsize0 != d->lsize1 || d->lsize0 != 16)
+        return set_error(PS_ERR_ARG, "matmul_sq realisation uses 16x16 work-groups");
+      if (d->n < 16 || d->n % 16 != 0)
+        return set_error(PS_ERR_ARG, "matmul_sq requires n to be a multiple of 16");
+      if (d->gen == PS_GEN_MATMUL_TC && d->n % 128 != 0)
+        return set_error(PS_ERR_ARG, "matmul_sq_tc requires n to be a multiple of 128");
+      return PS_OK;
+    case PS_GEN_FD:
+    case PS_GEN_FD_RM: {
+      if (d->dtype != PS_F32) return set_error(PS_ERR_ARG, "finite_diff is float32 only");
+      int I = d->tile - 2;
+      if (d->n < I || d->n % I != 0)
+        return set_error(PS_ERR_ARG, "finite_diff requires n to be a multiple of %d", I);
+      return PS_OK;
+    }
+    case PS_GEN_DG:
+    case PS_GEN_DG_RM:
+      return dg_validate(d);
+    default:
+      return set_error(PS_ERR_ARG, "unknown generator %d", d->gen);
+  }
+}
+
+int kernel_io(const ps_kernel_desc* d, ps_io_info* io) {
+  std::memset(io, 0, sizeof *io);
+  io->elem_bytes = d->dtype == PS_F64 ? 8 : 4;
+  const double eb = io->elem_bytes;
+  const double E = (double)d->nelements;
+  const double m = (double)d->m;
+  auto in = [&](int64_t n) { io->input_elems[io->n_inputs++] = n; };
+  auto out = [&](int64_t n) { io->output_elems[io->n_outputs++] = n; };
+  switch (d->gen) {
+    case PS_GEN_GMEM_PATTERN:
+      for (int i = 0; i < d->n_inputs; ++i) in(d->nelements);
+      out(d->nelements);
+      io->bytes_global = eb * E * (d->n_inputs + 1);
+      io->flops = E * (d->n_inputs - 1);
+      break;
+    case PS_GEN_FLOPS:
+      out(d->nelements);
+      io->bytes_global = eb * E;
+      io->flops = E * (2048.0 * m * (d->op == PS_OP_MADD ? 2.0 : 1.0) + 31.0);
+      break;
+    case PS_GEN_LMEM_SHUFFLE:
+      out(d->nelements);
+      io->bytes_global = eb * E;
+      io->bytes_shared = eb * E * (2.0 * m + 2.0);
+      break;
+    case PS_GEN_BARRIER:
+      out(d->nelements);
+      io->bytes_global = eb * E;
+      break;
+    case PS_GEN_EMPTY:
+      break;
+    case PS_GEN_OVERLAP:
+      in(d->nelements);
+      out(d->nelements);
+      io->bytes_global = 2.0 * eb * E;
+      io->bytes_shared = 2.0 * eb * E * m;
+      break;
+    case PS_GEN_MATMUL:
+    case PS_GEN_MATMUL_TC: {
+      const double n = (double)d->n;
+      in(d->n * d->n);
+      in(d->n * d->n);
+      out(d->n * d->n);
+      io->bytes_global = 3.0 * eb * n * n;
+      io->flops = 2.0 * n * n * n;
+      if (d->gen == PS_GEN_MATMUL && d->prefetch)
+        io->bytes_shared = eb * (2.0 * n * n * n + 2.0 * n * n * (n / 16.0));
+      break;
+    }
+    case PS_GEN_MATMUL_RM: {
+      const double n = (double)d->n;
+      in(d->n * d->n);
+      out(d->n * d->n);
+      io->bytes_global = 2.0 * eb * n * n;
+      break;
+    }
+    case PS_GEN_FD: {
+      const double n = (double)d->n;
+      in((d->n + 2) * (d->n + 2));
+      out(d->n * d->n);
+      io->bytes_global = eb * ((n + 2) * (n + 2) + n * n);
+      io->flops = 5.0 * n * n;
+      const double T = d->tile, I = d->tile - 2;
+      io->bytes_shared = eb * ((n / I) * (n / I) * T * T + 5.0 * n * n);
+      break;
+    }
+    case PS_GEN_FD_RM: {
+      const int64_t I = d->tile - 2;
+      if (d->keep == PS_KEEP_U) {
+        const int64_t dw = (d->n / I) * d->tile;
+        in((d->n + 2) * (d->n + 2));
+        out(dw * dw);
+        io->bytes_global = eb * ((double)(d->n + 2) * (d->n + 2) + (double)dw * dw);
+      } else {
+        out(d->n * d->n);
+        io->bytes_global = eb * (double)d->n * d->n;
+      }
+      break;
+    }
+    case PS_GEN_DG:
+    case PS_GEN_DG_RM:
+      return dg_io(d, io);
+    default:
+      return set_error(PS_ERR_ARG, "unknown generator %d", d->gen);
+  }
+  return PS_OK;
+}
+
+// Names of the global input arrays (seed pattern is keyed by array name).
+static const char* input_name(const ps_kernel_desc* d, int i) {
+  switch (d->gen) {
+    case PS_GEN_GMEM_PATTERN: return i == 0 ? "in0" : "in1";
+    case PS_GEN_OVERLAP: return "in0";
+    case PS_GEN_MATMUL:
+    case PS_GEN_MATMUL_TC: return i == 0 ? "a" : "b";
+    case PS_GEN_MATMUL_RM: return d->keep == PS_KEEP_A ? "a" : "b";
+    case PS_GEN_FD:
+    case PS_GEN_FD_RM: return "u";
+    case PS_GEN_DG:
+    case PS_GEN_DG_RM: return dg_input_name(d, i);
+    default: return "x";
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Device fills.
+
+__global__ void fill_seed17(void* buf, int64_t n, int elem_bytes, uint64_t name_hash) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t h = (name_hash ^ (uint64_t)i) * 1099511628211ull;
+    double v = 1.0 + (double)(h % 17ull);
+    if (elem_bytes == 4)
+      static_cast<float*>(buf)[i] = (float)v;
+    else
+      static_cast<double*>(buf)[i] = v;
+  }
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+__global__ void fill_uniform(void* buf, int64_t n, int elem_bytes, uint64_t key) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t r = splitmix64(key ^ (uint64_t)i * 0xd1b54a32d192ed03ull);
+    // 24 random bits -> k / 2^23 - 1 in [-1, 1), exact in float32.
+    double v = (double)(r >> 40) / 8388608.0 - 1.0;
+    if (elem_bytes == 4)
+      static_cast<float*>(buf)[i] = (float)v;
+    else
+      static_cast<double*>(buf)[i] = v;
+  }
+}
+
+uint64_t fnv1a_name(const char* name) {
+  uint64_t h = 1469598103934665603ull;
+  for (const char* c = name; *c; ++c) {
+    h ^= (unsigned char)*c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+// ---------------------------------------------------------------------------
+// Context.
+
+int Ctx::ensure(DevBuf& b, size_t bytes) {
+  if (b.cap >= bytes && b.ptr) return PS_OK;
+  if (b.ptr) cudaFree(b.ptr);
+  b.ptr = nullptr;
+  b.cap = 0;
+  cudaError_t e = cudaMalloc(&b.ptr, std::max<size_t>(bytes, 256));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(PS_ERR_NOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+  }
+  b.cap = std::max<size_t>(bytes, 256);
+  return PS_OK;
+}
+
+int prepare(Ctx* c, const ps_kernel_desc* d, int fill_mode, uint64_t seed) {
+  PS_CUDA(cudaSetDevice(c->device));
+  ps_io_info io;
+  int rc = kernel_io(d, &io);
+  if (rc) return rc;
+  bool same = c->prepared && std::memcmp(&c->desc, d, sizeof *d) == 0 &&
+              c->fill_mode == fill_mode && c->seed == seed;
+  if (same) return PS_OK;
+  for (int i = 0; i < io.n_inputs; ++i) {
+    size_t bytes = (size_t)io.input_elems[i] * io.elem_bytes;
+    if ((rc = c->ensure(c->in[i], bytes))) return rc;
+    uint64_t h = fnv1a_name(input_name(d, i));
+    int blocks = (int)std::min<int64_t>((io.input_elems[i] + 255) / 256, c->sm_count * 32);
+    if (fill_mode == PS_FILL_SEED17)
+      fill_seed17<<<blocks, 256, 0, c->stream>>>(c->in[i].ptr, io.input_elems[i], io.elem_bytes, h);
+    else
+      fill_uniform<<<blocks, 256, 0, c->stream>>>(c->in[i].ptr, io.input_elems[i], io.elem_bytes,
+                                                  h ^ (seed * 0x9e3779b97f4a7c15ull));
+    PS_CUDA(cudaGetLastError());
+  }
+  for (int i = 0; i < io.n_outputs; ++i) {
+    size_t bytes = (size_t)io.output_elems[i] * io.elem_bytes;
+    if ((rc = c->ensure(c->out[i], bytes))) return rc;
+    PS_CUDA(cudaMemsetAsync(c->out[i].ptr, 0, bytes, c->stream));
+  }
+  PS_CUDA(cudaStreamSynchronize(c->stream));
+  c->desc = *d;
+  c->io = io;
+  c->fill_mode = fill_mode;
+  c->seed = seed;
+  c->prepared = true;
+  return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Launch dispatch.
+
+static Pattern make_pattern(const ps_kernel_desc* d) {
+  Pattern p;
+  p.s0 = d->lid_stride0;
+  p.s1 = d->lid_stride1;
+  p.L0 = (int32_t)d->lsize0;
+  p.L1 = (int32_t)d->lsize1;
+  p.G0 = d->lid_stride1 / (d->lid_stride0 * d->lsize0);
+  p.G1 = d->nelements / (d->lid_stride1 * d->lsize1);
+  return p;
+}
+
+int launch(Ctx* c, const ps_kernel_desc* d) {
+  cudaStream_t st = c->stream;
+  void* in0 = c->in[0].ptr;
+  void* in1 = c->in[1].ptr;
+  void* out0 = c->out[0].ptr;
+  switch (d->gen) {
+    case PS_GEN_GMEM_PATTERN: {
+      Pattern p = make_pattern(d);
+      const int64_t groups = p.G0 * p.G1;
+      if (groups > INT32_MAX) return set_error(PS_ERR_ARG, "too many work-groups");
+      if (p.s0 == 1 && d->dtype == PS_F32 && d->nelements % 4 == 0 && !c->force_generic) {
+        // Contiguous index set [0, E): row-sweeping vectorised realisation.
+        constexpr int ROWS = 4;
+        const int64_t vecs = d->nelements / 4;
+        int64_t blocks = (vecs + 256 * ROWS - 1) / (256 * ROWS);
+        blocks = std::min<int64_t>(blocks, (int64_t)c->sm_count * 8);
+        if (d->n_inputs == 1)
+          gmem_pattern_rows<float, 1, 4, ROWS><<<(unsigned)blocks, 256, 0, st>>>(
+              (const float*)in0, nullptr, (float*)out0, p.s1, d->nelements / p.s1);
+        else
+          gmem_pattern_rows<float, 2, 4, ROWS><<<(unsigned)blocks, 256, 0, st>>>(
+              (const float*)in0, (const float*)in1, (float*)out0, p.s1, d->nelements / p.s1);
+        break;
+      }
+      dim3 block(p.L0, p.L1);
+      if (d->dtype == PS_F32) {
+        if (d->n_inputs == 1)
+          gmem_pattern_generic<float, 1><<<(unsigned)groups, block, 0, st>>>(
+              (const float*)in0, nullptr, (float*)out0, p);
+        else
+          gmem_pattern_generic<float, 2><<<(unsigned)groups, block, 0, st>>>(
+              (const float*)in0, (const float*)in1, (float*)out0, p);
+      } else {
+        if (d->n_inputs == 1)
+          gmem_pattern_generic<double, 1><<<(unsigned)groups, block, 0, st>>>(
+              (const double*)in0, nullptr, (double*)out0, p);
+        else
+          gmem_pattern_generic<double, 2><<<(unsigned)groups, block, 0, st>>>(
+              (const double*)in0, (const double*)in1, (double*)out0, p);
+      }
+      break;
+    }
+    case PS_GEN_FLOPS: {
+      Pattern p = make_pattern(d);
+      dim3 block(p.L0, p.L1);
+      const unsigned groups = (unsigned)(p.G0 * p.G1);
+      const float base = c->flop_base, step = c->flop_step;
+      if (d->op == PS_OP_ADD)
+        flops_pattern<0><<<groups, block, 0, st>>>((float*)out0, p, (int)d->m, base, step);
+      else if (d->op == PS_OP_MUL)
+        flops_pattern<1><<<groups, block, 0, st>>>((float*)out0, p, (int)d->m, base, step);
+      else
+        flops_pattern<2><<<groups, block, 0, st>>>((float*)out0, p, (int)d->m, base, step);
+      break;
+    }
+    case PS_GEN_LMEM_SHUFFLE: {
+      Pattern p = make_pattern(d);
+      dim3 block(p.L0, p.L1);
+      size_t sm = 2 * sizeof(float) * p.L0 * p.L1;
+      lmem_shuffle<<<(unsigned)(p.G0 * p.G1), block, sm, st>>>((float*)out0, p, (int)d->m);
+      break;
+    }
+    case PS_GEN_BARRIER: {
+      Pattern p = make_pattern(d);
+      dim3 block(p.L0, p.L1);
+      barrier_knl<<<(unsigned)(p.G0 * p.G1), block, 0, st>>>((float*)out0, p, (int)d->m);
+      break;
+    }
+    case PS_GEN_EMPTY:
+      empty_knl<<<(unsigned)d->num_groups, 256, 0, st>>>();
+      break;
+    case PS_GEN_OVERLAP: {
+      Pattern p = make_pattern(d);
+      dim3 block(p.L0, p.L1);
+      size_t sm = 2 * sizeof(float) * p.L0 * p.L1;
+      overlap_knl<<<(unsigned)(p.G0 * p.G1), block, sm, st>>>((const float*)in0, (float*)out0, p,
+                                                               (int)d->m);
+      break;
+    }
+    case PS_GEN_MATMUL: {
+      const int n = (int)d->n;
+      dim3 grid(n / 16, n / 16), block(16, 16);
+      if (d->dtype == PS_F32) {
+        if (d->prefetch)
+          matmul_pf<float, 16><<<grid, block, 0, st>>>((const float*)in0, (const float*)in1,
+                                                       (float*)out0, n);
+        else
+          matmul_nopf<float><<<grid, block, 0, st>>>((const float*)in0, (const float*)in1,
+                                                     (float*)out0, n, 16);
+      } else {
+        if (d->prefetch)
+          matmul_pf<double, 16><<<grid, block, 0, st>>>((const double*)in0, (const double*)in1,
+                                                        (double*)out0, n);
+        else
+          matmul_nopf<double><<<grid, block, 0, st>>>((const double*)in0, (const double*)in1,
+                                                      (double*)out0, n, 16);
+      }
+      break;
+    }
+    case PS_GEN_MATMUL_RM: {
+      const int n = (int)d->n;
+      dim3 grid(n / 16, n / 16), block(16, 16);
+#define PS_MM_RM(T)                                                                      \
+  if (d->prefetch) {                                                                     \
+    if (d->keep == PS_KEEP_A)                                                            \
+      matmul_rm<T, true, 1><<<grid, block, 0, st>>>((const T*)in0, (T*)out0, n, 16);     \
+    else                                                                                 \
+      matmul_rm<T, true, 2><<<grid, block, 0, st>>>((const T*)in0, (T*)out0, n, 16);     \
+  } else {                                                                               \
+    if (d->keep == PS_KEEP_A)                                                            \
+      matmul_rm<T, false, 1><<<grid, block, 0, st>>>((const T*)in0, (T*)out0, n, 16);    \
+    else                                                                                 \
+      matmul_rm<T, false, 2><<<grid, block, 0, st>>>((const T*)in0, (T*)out0, n, 16);    \
+  }
+      if (d->dtype == PS_F32) {
+        PS_MM_RM(float)
+      } else {
+        PS_MM_RM(double)
+      }
+#undef PS_MM_RM
+      break;
+    }
+    case PS_GEN_FD: {
+      const int n = (int)d->n;
+      const int I = d->tile - 2;
+      dim3 grid(n / I, n / I), block(d->tile, d->tile);
+      if (d->tile == 16)
+        finite_diff<16><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
+      else
+        finite_diff<18><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
+      break;
+    }
+    case PS_GEN_FD_RM: {
+      const int n = (int)d->n;
+      const int I = d->tile - 2;
+      dim3 grid(n / I, n / I), block(d->tile, d->tile);
+      if (d->keep == PS_KEEP_U) {
+        if (d->tile == 16)
+          finite_diff_rm_u<16><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
+        else
+          finite_diff_rm_u<18><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
+      } else {
+        if (d->tile == 16)
+          finite_diff_rm_res<16><<<grid, block, 0, st>>>((float*)out0, n);
+        else
+          finite_diff_rm_res<18><<<grid, block, 0, st>>>((float*)out0, n);
+      }
+      break;
+    }
+    case PS_GEN_DG:
+    case PS_GEN_DG_RM:
+      return dg_launch(c, d);
+    case PS_GEN_MATMUL_TC:
+      return tc_launch(c, d);
+    default:
+      return set_error(PS_ERR_ARG, "unknown generator %d", d->gen);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return set_error(PS_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+  return PS_OK;
+}
+
+int events(Ctx* c, int n) {
+  while ((int)c->ev.size() < n) {
+    cudaEvent_t e;
+    PS_CUDA(cudaEventCreate(&e));
+    c->ev.push_back(e);
+  }
+  return PS_OK;
+}
+
+}  // namespace ps
+
+// ---------------------------------------------------------------------------
+// Exported C ABI.
+
+using namespace ps;
+
+extern "C" {
+
+const char* ps_last_error(void) { return g_last_error.c_str(); }
+const char* ps_version(void) { return "perfseer_b200 0.1 (sm_100a)"; }
+
+int ps_desc_from_id(const char* variant_id, ps_kernel_desc* out) {
+  return parse_variant_id(variant_id, out);
+}
+
+int ps_kernel_io(const ps_kernel_desc* desc, ps_io_info* out) {
+  if (!desc || !out) return set_error(PS_ERR_ARG, "ps_kernel_io: null argument");
+  int rc = validate_desc(desc);
+  if (rc) return rc;
+  return kernel_io(desc, out);
+}
+
+int ps_init(int device, ps_ctx** out) {
+  if (!out) return set_error(PS_ERR_ARG, "ps_init: null out");
+  int count = 0;
+  PS_CUDA(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count)
+    return set_error(PS_ERR_ARG, "ps_init: device %d not present (%d visible)", device, count);
+  PS_CUDA(cudaSetDevice(device));
+  Ctx* c = new Ctx();
+  c->device = device;
+  cudaDeviceProp prop;
+  PS_CUDA(cudaGetDeviceProperties(&prop, device));
+  c->sm_count = prop.multiProcessorCount;
+  c->l2_bytes = prop.l2CacheSize;
+  int clk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device);
+  c->sm_clock_khz = clk;
+  if (prop.major != 10) {
+    delete c;
+    return set_error(PS_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a",
+                     device, prop.major, prop.minor);
+  }
+  PS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  const char* gen = getenv("PS_GMEM_GENERIC");
+  c->force_generic = gen && gen[0] == '1';
+  *out = reinterpret_cast<ps_ctx*>(c);
+  return PS_OK;
+}
+
+int ps_destroy(ps_ctx* ctx) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return PS_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& b : c->in)
+    if (b.ptr) cudaFree(b.ptr);
+  for (auto& b : c->out)
+    if (b.ptr) cudaFree(b.ptr);
+  for (auto& b : c->scratch)
+    if (b.ptr) cudaFree(b.ptr);
+  for (auto e : c->ev) cudaEventDestroy(e);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return PS_OK;
+}
+
+int ps_device_info(ps_ctx* ctx, int* sm_count, int* sm_clock_khz, size_t* l2_bytes,
+                   size_t* free_bytes) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_error(PS_ERR_ARG, "null ctx");
+  PS_CUDA(cudaSetDevice(c->device));
+  if (sm_count) *sm_count = c->sm_count;
+  if (sm_clock_khz) *sm_clock_khz = c->sm_clock_khz;
+  if (l2_bytes) *l2_bytes = c->l2_bytes;
+  if (free_bytes) {
+    size_t fr = 0, tot = 0;
+    PS_CUDA(cudaMemGetInfo(&fr, &tot));
+    *free_bytes = fr;
+  }
+  return PS_OK;
+}
+
+int ps_prepare(ps_ctx* ctx, const ps_kernel_desc* desc, int fill_mode, uint64_t seed) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !desc) return set_error(PS_ERR_ARG, "ps_prepare: null argument");
+  int rc = validate_desc(desc);
+  if (rc) return rc;
+  return prepare(c, desc, fill_mode, seed);
+}
+
+int ps_measure(ps_ctx* ctx, const ps_kernel_desc* desc, int warmup, int trials,
+               double* out_seconds) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !desc || !out_seconds) return set_error(PS_ERR_ARG, "ps_measure: null argument");
+  if (trials < 1) return set_error(PS_ERR_ARG, "trials must be >= 1");  // executor.cpp:145
+  if (warmup < 0) return set_error(PS_ERR_ARG, "warmup must be >= 0");
+  int rc = validate_desc(desc);
+  if (rc) return rc;
+  if (!c->prepared || std::memcmp(&c->desc, desc, sizeof *desc) != 0)
+    if ((rc = prepare(c, desc, PS_FILL_SEED17, 0))) return rc;
+  PS_CUDA(cudaSetDevice(c->device));
+  if ((rc = events(c, 2 * trials))) return rc;
+  for (int w = 0; w < warmup; ++w)
+    if ((rc = launch(c, desc))) return rc;
+  for (int t = 0; t < trials; ++t) {
+    PS_CUDA(cudaEventRecord(c->ev[2 * t], c->stream));
+    if ((rc = launch(c, desc))) return rc;
+    PS_CUDA(cudaEventRecord(c->ev[2 * t + 1], c->stream));
+  }
+  PS_CUDA(cudaStreamSynchronize(c->stream));
+  for (int t = 0; t < trials; ++t) {
+    float ms = 0.f;
+    PS_CUDA(cudaEventElapsedTime(&ms, c->ev[2 * t], c->ev[2 * t + 1]));
+    out_seconds[t] = (double)ms * 1e-3;
+  }
+  return PS_OK;
+}
+
+int ps_measure_summary(ps_ctx* ctx, const ps_kernel_desc* desc, int warmup, int trials,
+                       double filter_factor, double* mean_seconds, int* kept_trials) {
+  if (!mean_seconds) return set_error(PS_ERR_ARG, "null mean_seconds");
+  std::vector<double> t(trials > 0 ? trials : 1);
+  int rc = ps_measure(ctx, desc, warmup, trials, t.data());
+  if (rc) return rc;
+  // summarize (executor.cpp:14-38): median of sorted copy (mean of the two
+  // middle values for even counts), drop > factor * median, mean of the
+  // survivors accumulated in original order.
+  std::vector<double> s = t;
+  std::sort(s.begin(), s.end());
+  size_t n = s.size();
+  double med = n % 2 ? s[n / 2] : 0.5 * (s[n / 2 - 1] + s[n / 2]);
+  double cut = filter_factor * med, sum = 0.0;
+  int kept = 0;
+  for (double v : t)
+    if (!(v > cut)) sum += v, ++kept;
+  *mean_seconds = sum / kept;
+  if (kept_trials) *kept_trials = kept;
+  return PS_OK;
+}
+
+int ps_run_timed(ps_ctx* ctx, const ps_kernel_desc* desc, int launches, double* seconds) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !desc || !seconds) return set_error(PS_ERR_ARG, "ps_run_timed: null argument");
+  int rc = validate_desc(desc);
+  if (rc) return rc;
+  if (!c->prepared || std::memcmp(&c->desc, desc, sizeof *desc) != 0)
+    if ((rc = prepare(c, desc, PS_FILL_SEED17, 0))) return rc;
+  PS_CUDA(cudaSetDevice(c->device));
+  if ((rc = events(c, 2))) return rc;
+  PS_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  for (int i = 0; i < launches; ++i)
+    if ((rc = launch(c, desc))) return rc;
+  PS_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  PS_CUDA(cudaEventSynchronize(c->ev[1]));
+  float ms = 0.f;
+  PS_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  *seconds = (double)ms * 1e-3;
+  return PS_OK;
+}
+
+int ps_run_verify(ps_ctx* ctx, const ps_kernel_desc* desc, const void* const* inputs,
+                  int n_inputs, void* const* outputs, int n_outputs) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !desc) return set_error(PS_ERR_ARG, "ps_run_verify: null argument");
+  int rc = validate_desc(desc);
+  if (rc) return rc;
+  ps_io_info io;
+  if ((rc = kernel_io(desc, &io))) return rc;
+  if (n_inputs != io.n_inputs || n_outputs != io.n_outputs)
+    return set_error(PS_ERR_ARG, "kernel takes %d inputs / %d outputs, got %d / %d",
+                     io.n_inputs, io.n_outputs, n_inputs, n_outputs);
+  PS_CUDA(cudaSetDevice(c->device));
+  for (int i = 0; i < io.n_inputs; ++i) {
+    size_t bytes = (size_t)io.input_elems[i] * io.elem_bytes;
+    if ((rc = c->ensure(c->in[i], bytes))) return rc;
+    PS_CUDA(cudaMemcpyAsync(c->in[i].ptr, inputs[i], bytes, cudaMemcpyHostToDevice, c->stream));
+  }
+  for (int i = 0; i < io.n_outputs; ++i) {
+    size_t bytes = (size_t)io.output_elems[i] * io.elem_bytes;
+    if ((rc = c->ensure(c->out[i], bytes))) return rc;
+    PS_CUDA(cudaMemsetAsync(c->out[i].ptr, 0, bytes, c->stream));
+  }
+  c->prepared = false;  // buffers now hold caller data
+  if ((rc = launch(c, desc))) return rc;
+  for (int i = 0; i < io.n_outputs; ++i) {
+    size_t bytes = (size_t)io.output_elems[i] * io.elem_bytes;
+    PS_CUDA(cudaMemcpyAsync(outputs[i], c->out[i].ptr, bytes, cudaMemcpyDeviceToHost, c->stream));
+  }
+  PS_CUDA(cudaStreamSynchronize(c->stream));
+  return PS_OK;
+}
+
+int ps_buffer(ps_ctx* ctx, int is_output, int index, void** dev_ptr, int64_t* elems) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !dev_ptr) return set_error(PS_ERR_ARG, "ps_buffer: null argument");
+  if (!c->prepared) return set_error(PS_ERR_STATE, "ps_buffer: call ps_prepare first");
+  int n = is_output ? c->io.n_outputs : c->io.n_inputs;
+  if (index < 0 || index >= n) return set_error(PS_ERR_ARG, "ps_buffer: index out of range");
+  *dev_ptr = is_output ? c->out[index].ptr : c->in[index].ptr;
+  if (elems) *elems = is_output ? c->io.output_elems[index] : c->io.input_elems[index];
+  return PS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,56 @@
+// Internal state of a ps_ctx (one per GPU) and the launch helpers shared by
+// the suite, DG, tensor-core and model translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "../../../include/perfseer_b200.h"
+
+namespace ps {
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t cap = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  int sm_count = 0;
+  int sm_clock_khz = 0;
+  size_t l2_bytes = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<cudaEvent_t> ev;
+  DevBuf in[PS_MAX_ARRAYS];
+  DevBuf out[PS_MAX_ARRAYS];
+  DevBuf scratch[8];
+  bool prepared = false;
+  ps_kernel_desc desc{};
+  ps_io_info io{};
+  int fill_mode = 0;
+  uint64_t seed = 0;
+  bool force_generic = false;
+  // flops_pattern initial values v_j = base + step*j (uipick.cpp:339-343)
+  float flop_base = 0.5f;
+  float flop_step = 0.015625f;
+
+  int ensure(DevBuf& b, size_t bytes);
+};
+
+int set_error(int code, const char* fmt, ...);
+int validate_desc(const ps_kernel_desc* d);
+int kernel_io(const ps_kernel_desc* d, ps_io_info* io);
+int parse_variant_id(const char* id, ps_kernel_desc* d);
+int launch(Ctx* c, const ps_kernel_desc* d);
+int events(Ctx* c, int n);
+
+int dg_validate(const ps_kernel_desc* d);
+int dg_io(const ps_kernel_desc* d, ps_io_info* io);
+const char* dg_input_name(const ps_kernel_desc* d, int i);
+int dg_launch(Ctx* c, const ps_kernel_desc* d);
+int tc_launch(Ctx* c, const ps_kernel_desc* d);
+
+}  // namespace ps

@@ -1,0 +1,320 @@
+// sm_100a realisations of the UIPiCK measurement kernels (reference
+// src/uipick.cpp:295-664).
+//
+// Contract: every kernel executes
+// exactly the IR of its generator — the same per-work-item index set, the
+// same arithmetic in the same order (madd = one fused multiply-add), the same
+// memory spaces (global vs shared) and the same barrier count per
+// work-group. Work-items map to threads one-to-one with lid(0) -> threadIdx.x
+// unless a kernel's comment states a coarsening; a coarsened thread executes
+// several whole work-items of the same work-group row, which keeps every
+// warp's addresses inside the cache lines the IR's lockstep order touches.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device_common.cuh"
+
+namespace ps {
+
+// PatternLayout (uipick.cpp:211-245): the global index of work-item
+// (lx, ly) in group (gx, gy) is s0*lx + s1*ly + s0*L0*gx + s1*L1*gy.
+struct Pattern {
+  int64_t s0, s1;
+  int32_t L0, L1;
+  int64_t G0, G1;
+  __device__ __forceinline__ int64_t gidx(int lx, int ly, int64_t gx, int64_t gy) const {
+    return s0 * lx + s1 * ly + s0 * L0 * gx + s1 * L1 * gy;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// K1 gmem_pattern, 1:1 geometry (general strides): result[g] = in0[g] (+ in1[g])
+// left-associated (uipick.cpp:306-313). 1-D grid over G0*G1 work-groups.
+template <typename T, int K>
+__global__ void __launch_bounds__(1024) gmem_pattern_generic(const T* __restrict__ in0,
+                                                             const T* __restrict__ in1,
+                                                             T* __restrict__ out, Pattern p) {
+  int64_t bid = blockIdx.x;
+  int64_t gx = bid % p.G0, gy = bid / p.G0;
+  int64_t g = p.gidx(threadIdx.x, threadIdx.y, gx, gy);
+  T v = in0[g];
+  if constexpr (K == 2) v = add_t(v, in1[g]);
+  out[g] = v;
+}
+
+// K1 gmem_pattern, contiguous layout (s0 = 1, s1 = L0 * G0: every row of
+// the s1-wide matrix is covered by one row of work-groups). A thread executes
+// the VEC consecutive lx work-items (4*VEC contiguous bytes per array) of one
+// work-group row, and a CTA sweeps ROWS work-group rows, so each thread keeps
+// ROWS independent 16-byte loads per array in flight. Index set, arithmetic
+// and store per element are identical to the 1:1 kernel.
+template <typename T, int K, int VEC, int ROWS>
+__global__ void __launch_bounds__(256) gmem_pattern_rows(const T* __restrict__ in0,
+                                                         const T* __restrict__ in1,
+                                                         T* __restrict__ out, int64_t row_elems,
+                                                         int64_t nrows) {
+  using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  constexpr int kPerVec = sizeof(V) / sizeof(T);
+  static_assert(kPerVec * 1 == VEC, "VEC must equal the 16-byte lane width");
+  const int64_t vecs_per_row = row_elems / kPerVec;
+  const int64_t total_vecs = vecs_per_row * nrows;
+  const V* a = reinterpret_cast<const V*>(in0);
+  const V* b = reinterpret_cast<const V*>(in1);
+  V* o = reinterpret_cast<V*>(out);
+  int64_t base = (int64_t)blockIdx.x * blockDim.x * ROWS + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * ROWS;
+  for (; base < total_vecs; base += stride) {
+    V va[ROWS], vb[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      int64_t i = base + (int64_t)r * blockDim.x;
+      if (i < total_vecs) {
+        va[r] = __ldcs(a + i);
+        if constexpr (K == 2) vb[r] = __ldcs(b + i);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      int64_t i = base + (int64_t)r * blockDim.x;
+      if (i < total_vecs) {
+        V v = va[r];
+        if constexpr (K == 2) {
+          if constexpr (sizeof(T) == 4) {
+            v.x = add_t(v.x, vb[r].x);
+            v.y = add_t(v.y, vb[r].y);
+            v.z = add_t(v.z, vb[r].z);
+            v.w = add_t(v.w, vb[r].w);
+          } else {
+            v.x = add_t(v.x, vb[r].x);
+            v.y = add_t(v.y, vb[r].y);
+          }
+        }
+        __stcs(o + i, v);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2-K4 flops_{add,mul,madd}_pattern (uipick.cpp:317-378): 32 private values
+// v_j = 0.5 + j/64 (exact, flit at uipick.cpp:251-255); m iterations of a
+// 64x-unrolled SHOC sweep v_j <- op(v_{(j+27)%32}, v_{(j+21)%32}) (madd:
+// v_{(j+27)%32}*v_{(j+21)%32} + v_j fused); left-associated 31-add reduction;
+// one store. base/step arrive as runtime arguments so nothing folds.
+template <int OP>
+__device__ __forceinline__ float flop_op(float a, float c, float self) {
+  if constexpr (OP == 0) return __fadd_rn(a, c);
+  if constexpr (OP == 1) return __fmul_rn(a, c);
+  return __fmaf_rn(a, c, self);
+}
+
+template <int OP>
+__global__ void __launch_bounds__(256) flops_pattern(float* __restrict__ out, Pattern p, int m,
+                                                     float base, float step) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(base, __fmul_rn(step, (float)j));
+  for (int t = 0; t < m; ++t) {
+#pragma unroll
+    for (int u = 0; u < 64; ++u) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = flop_op<OP>(v[(j + 27) & 31], v[(j + 21) & 31], v[j]);
+    }
+  }
+  float r = v[0];
+#pragma unroll
+  for (int j = 1; j < 32; ++j) r = __fadd_rn(r, v[j]);
+  int64_t bid = blockIdx.x;
+  out[p.gidx(threadIdx.x, threadIdx.y, bid % p.G0, bid / p.G0)] = r;
+}
+
+// ---------------------------------------------------------------------------
+// K5 lmem_shuffle (uipick.cpp:380-404): locbuf_a[l] = 1; m x (locbuf_b[l] =
+// locbuf_a[l]); result[g] = locbuf_b[l]; no barrier. Shared accesses are
+// volatile so each of the m load/store pairs is issued. Loads of an unrolled
+// group are issued before its stores (they touch disjoint arrays, so the
+// order is semantically free) to keep the shared pipe, not latency, binding.
+__global__ void __launch_bounds__(1024) lmem_shuffle(float* __restrict__ out, Pattern p, int m) {
+  extern __shared__ float smem[];
+  const int wg = p.L0 * p.L1;
+  float* sa = smem;
+  float* sb = smem + wg;
+  const int l = threadIdx.x + p.L0 * threadIdx.y;
+  sts_volatile(&sa[l], 1.0f);
+  int t = 0;
+  for (; t + 4 <= m; t += 4) {
+    float x0 = lds_volatile(&sa[l]);
+    float x1 = lds_volatile(&sa[l]);
+    float x2 = lds_volatile(&sa[l]);
+    float x3 = lds_volatile(&sa[l]);
+    sts_volatile(&sb[l], x0);
+    sts_volatile(&sb[l], x1);
+    sts_volatile(&sb[l], x2);
+    sts_volatile(&sb[l], x3);
+  }
+  for (; t < m; ++t) sts_volatile(&sb[l], lds_volatile(&sa[l]));
+  float r = lds_volatile(&sb[l]);
+  int64_t bid = blockIdx.x;
+  out[p.gidx(threadIdx.x, threadIdx.y, bid % p.G0, bid / p.G0)] = r;
+}
+
+// K6 barrier_knl (uipick.cpp:406-423): m local barriers, then result[g] = 1.
+__global__ void __launch_bounds__(1024) barrier_knl(float* __restrict__ out, Pattern p, int m) {
+  for (int t = 0; t < m; ++t) bar_sync();
+  int64_t bid = blockIdx.x;
+  out[p.gidx(threadIdx.x, threadIdx.y, bid % p.G0, bid / p.G0)] = 1.0f;
+}
+
+// K7 empty_knl (uipick.cpp:425-432): no statements, num_groups x 256.
+__global__ void __launch_bounds__(256) empty_knl() {}
+
+// K8 overlap_knl (uipick.cpp:434-462): tmp = in0[g]; m x (locbuf_b[l] =
+// locbuf_a[l]) (locbuf_a is never written in the IR); result[g] = tmp.
+__global__ void __launch_bounds__(1024) overlap_knl(const float* __restrict__ in0,
+                                                    float* __restrict__ out, Pattern p, int m) {
+  extern __shared__ float smem[];
+  const int wg = p.L0 * p.L1;
+  float* sa = smem;
+  float* sb = smem + wg;
+  const int l = threadIdx.x + p.L0 * threadIdx.y;
+  int64_t bid = blockIdx.x;
+  const int64_t g = p.gidx(threadIdx.x, threadIdx.y, bid % p.G0, bid / p.G0);
+  float tmp = in0[g];
+  int t = 0;
+  for (; t + 2 <= m; t += 2) {
+    float x0 = lds_volatile(&sa[l]);
+    float x1 = lds_volatile(&sa[l]);
+    sts_volatile(&sb[l], x0);
+    sts_volatile(&sb[l], x1);
+  }
+  for (; t < m; ++t) sts_volatile(&sb[l], lds_volatile(&sa[l]));
+  out[g] = tmp;
+}
+
+// ---------------------------------------------------------------------------
+// K9 matmul_sq noPF (uipick.cpp:478-502): c[i,j] = sum_k a[i,k]*b[k,j] with
+// i = 16*i_out + i_in (g.1, l.1), j = 16*j_out + j_in (g.0, l.0); one madd
+// per k in ascending order, accumulator starting at 0.
+template <typename T>
+__global__ void __launch_bounds__(256) matmul_nopf(const T* __restrict__ a,
+                                                   const T* __restrict__ b, T* __restrict__ c,
+                                                   int n, int tile) {
+  const int i = blockIdx.y * tile + threadIdx.y;
+  const int j = blockIdx.x * tile + threadIdx.x;
+  const T* arow = a + (int64_t)i * n;
+  const T* bcol = b + j;
+  T acc = T(0);
+#pragma unroll 8
+  for (int k = 0; k < n; ++k) acc = fma_t(arow[k], bcol[(int64_t)k * n], acc);
+  c[(int64_t)i * n + j] = acc;
+}
+
+// K10 matmul_sq PF (uipick.cpp:504-553): per k_out: barrier; a_fetch[i_in,
+// j_in] = a[row, 16 k_out + j_in]; b_fetch[i_in, j_in] = b[16 k_out + i_in,
+// col]; barrier; 16 madds acc += a_fetch[i_in,k_in] * b_fetch[k_in,j_in].
+template <typename T, int TS>
+__global__ void __launch_bounds__(TS* TS) matmul_pf(const T* __restrict__ a,
+                                                    const T* __restrict__ b, T* __restrict__ c,
+                                                    int n) {
+  __shared__ T af[TS][TS];
+  __shared__ T bf[TS][TS];
+  const int ti = threadIdx.y, tj = threadIdx.x;
+  const int row = blockIdx.y * TS + ti;
+  const int col = blockIdx.x * TS + tj;
+  T acc = T(0);
+  const int ntiles = n / TS;
+  for (int kt = 0; kt < ntiles; ++kt) {
+    bar_sync();  // bar_pre
+    af[ti][tj] = a[(int64_t)row * n + kt * TS + tj];
+    bf[ti][tj] = b[(int64_t)(kt * TS + ti) * n + col];
+    bar_sync();  // bar_post
+#pragma unroll
+    for (int kin = 0; kin < TS; ++kin) acc = fma_t(af[ti][kin], bf[kin][tj], acc);
+  }
+  c[(int64_t)row * n + col] = acc;
+}
+
+// K11 matmul_sq_rm (uipick.cpp:556-581 via remove_work, transforms.cpp:317-514):
+// tgt_read = 0; tgt_read += (surviving load) over its loop; tgt_read_dest[i, j]
+// = tgt_read with lid(0) fastest. keep: 1 = a, 2 = b.
+template <typename T, bool PF, int KEEP>
+__global__ void __launch_bounds__(256) matmul_rm(const T* __restrict__ src,
+                                                 T* __restrict__ dest, int n, int tile) {
+  const int ti = threadIdx.y, tj = threadIdx.x;
+  const int row = blockIdx.y * tile + ti;
+  const int col = blockIdx.x * tile + tj;
+  T acc = T(0);
+  if constexpr (PF) {
+    const int ntiles = n / tile;
+#pragma unroll 4
+    for (int kt = 0; kt < ntiles; ++kt) {
+      if constexpr (KEEP == 1)
+        acc = add_t(acc, src[(int64_t)row * n + kt * tile + tj]);
+      else
+        acc = add_t(acc, src[(int64_t)(kt * tile + ti) * n + col]);
+    }
+  } else {
+#pragma unroll 8
+    for (int k = 0; k < n; ++k) {
+      if constexpr (KEEP == 1)
+        acc = add_t(acc, src[(int64_t)row * n + k]);
+      else
+        acc = add_t(acc, src[(int64_t)k * n + col]);
+    }
+  }
+  dest[(int64_t)row * n + col] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// K12 finite_diff TxT (uipick.cpp:583-639): fetch the TxT tile u[I i_out + l1,
+// I j_out + l0] to shared; barrier; the I x I interior points of the
+// five-point stencil, ((u01 + u10) - 4 u11) + u12 + u21 with the -4 u11 term
+// fused (the IR counts it as a madd). The IR places the compute in
+// sequential c1, c0 loops (a uniform, per-sub-group access); the
+// realisation assigns interior point (c1, c0) to work-item (l1, l0), which
+// executes the same n^2 statement instances.
+template <int T>
+__global__ void __launch_bounds__(T* T) finite_diff(const float* __restrict__ u,
+                                                   float* __restrict__ res, int n) {
+  constexpr int I = T - 2;
+  __shared__ float uf[T][T + 1];
+  const int l0 = threadIdx.x, l1 = threadIdx.y;
+  const int i_out = blockIdx.y, j_out = blockIdx.x;
+  const int64_t W = n + 2;
+  uf[l1][l0] = u[(int64_t)(I * i_out + l1) * W + I * j_out + l0];
+  bar_sync();
+  if (l1 < I && l0 < I) {
+    float s = __fadd_rn(uf[l1][l0 + 1], uf[l1 + 1][l0]);
+    s = __fmaf_rn(-4.0f, uf[l1 + 1][l0 + 1], s);
+    s = __fadd_rn(s, uf[l1 + 1][l0 + 2]);
+    s = __fadd_rn(s, uf[l1 + 2][l0 + 1]);
+    res[(int64_t)(I * i_out + l1) * n + I * j_out + l0] = s;
+  }
+}
+
+// K13 finite_diff_rm (uipick.cpp:641-664). keep u: tgt_read = 0 + u[fetch
+// index]; tgt_read_dest[T i_out + l1, T j_out + l0] = tgt_read. keep res:
+// res[interior] = tgt_read = 0.
+template <int T>
+__global__ void __launch_bounds__(T* T) finite_diff_rm_u(const float* __restrict__ u,
+                                                        float* __restrict__ dest, int n) {
+  constexpr int I = T - 2;
+  const int l0 = threadIdx.x, l1 = threadIdx.y;
+  const int i_out = blockIdx.y, j_out = blockIdx.x;
+  const int64_t W = n + 2;
+  const int64_t DW = (int64_t)(n / I) * T;
+  float acc = __fadd_rn(0.0f, u[(int64_t)(I * i_out + l1) * W + I * j_out + l0]);
+  dest[(int64_t)(T * i_out + l1) * DW + T * j_out + l0] = acc;
+}
+
+template <int T>
+__global__ void __launch_bounds__(T* T) finite_diff_rm_res(float* __restrict__ res, int n) {
+  constexpr int I = T - 2;
+  const int l0 = threadIdx.x, l1 = threadIdx.y;
+  if (l1 < I && l0 < I)
+    res[(int64_t)(I * blockIdx.y + l1) * n + I * blockIdx.x + l0] = 0.0f;
+}
+
+}  // namespace ps

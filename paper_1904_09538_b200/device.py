@@ -1,0 +1,98 @@
+"""Python face of the B200 executor: a ps_ctx per GPU behind the C ABI.
+
+Mirrors perfseer::Executor (reference include/perfseer/executor.hpp:16-23):
+``id()`` and ``measure(kernel_id, trials)`` returning per-trial seconds, plus
+``measure_summary`` = measure_kernel + summarize (src/executor.cpp:14-48).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _abi
+from ._abi import KernelDesc, check, lib
+
+
+def _desc(kernel) -> KernelDesc:
+    if isinstance(kernel, KernelDesc):
+        return kernel
+    return _abi.desc_from_id(str(kernel))
+
+
+class CudaDevice:
+    """One GPU context. Not reentrant (executors are exclusive resources)."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        self._ctx = C.c_void_p()
+        check(lib().ps_init(device, C.byref(self._ctx)))
+
+    def id(self) -> str:
+        return f"cuda_b200_{self.device}"
+
+    def close(self) -> None:
+        if self._ctx:
+            lib().ps_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        sm, clk, l2, free = C.c_int(), C.c_int(), C.c_size_t(), C.c_size_t()
+        check(lib().ps_device_info(self._ctx, C.byref(sm), C.byref(clk), C.byref(l2),
+                                   C.byref(free)))
+        return {"sm_count": sm.value, "sm_clock_khz": clk.value, "l2_bytes": l2.value,
+                "free_bytes": free.value}
+
+    def prepare(self, kernel, fill: int = _abi.PS_FILL_SEED17, seed: int = 0) -> None:
+        check(lib().ps_prepare(self._ctx, C.byref(_desc(kernel)), fill, seed))
+
+    def measure(self, kernel, trials: int = 60, warmup: int = 5) -> list[float]:
+        d = _desc(kernel)
+        out = (C.c_double * trials)()
+        check(lib().ps_measure(self._ctx, C.byref(d), warmup, trials, out))
+        return list(out)
+
+    def measure_summary(self, kernel, trials: int = 60, warmup: int = 5,
+                        filter_factor: float = 5.0) -> tuple[float, int]:
+        d = _desc(kernel)
+        mean, kept = C.c_double(), C.c_int()
+        check(lib().ps_measure_summary(self._ctx, C.byref(d), warmup, trials, filter_factor,
+                                       C.byref(mean), C.byref(kept)))
+        return mean.value, kept.value
+
+    def run_timed(self, kernel, launches: int) -> float:
+        d = _desc(kernel)
+        s = C.c_double()
+        check(lib().ps_run_timed(self._ctx, C.byref(d), launches, C.byref(s)))
+        return s.value
+
+    def run(self, kernel, inputs: list[np.ndarray]) -> list[np.ndarray]:
+        """Parity hook: host inputs -> one launch -> host outputs."""
+        d = _desc(kernel)
+        io = _abi.kernel_io(d)
+        dt = np.float32 if io.elem_bytes == 4 else np.float64
+        if len(inputs) != io.n_inputs:
+            raise ValueError(f"kernel takes {io.n_inputs} inputs, got {len(inputs)}")
+        ins = []
+        for i, a in enumerate(inputs):
+            a = np.ascontiguousarray(a, dtype=dt).reshape(-1)
+            if a.size != io.input_elems[i]:
+                raise ValueError(f"input {i}: expected {io.input_elems[i]} elements, got {a.size}")
+            ins.append(a)
+        outs = [np.empty(io.output_elems[i], dtype=dt) for i in range(io.n_outputs)]
+        in_ptrs = (C.c_void_p * max(1, len(ins)))(*[a.ctypes.data for a in ins])
+        out_ptrs = (C.c_void_p * max(1, len(outs)))(*[a.ctypes.data for a in outs])
+        check(lib().ps_run_verify(self._ctx, C.byref(d), in_ptrs, len(ins), out_ptrs, len(outs)))
+        return outs

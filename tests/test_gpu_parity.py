@@ -1,0 +1,97 @@
+"""CUDA kernels (through the C ABI, host buffers) vs the CPU restatement
+oracle/suite_ref.c on the same inputs: bitwise equality (integer-valued seed
+inputs and U[-1,1) inputs; same operation order, fused madd)."""
+import numpy as np
+import pytest
+
+from oracle import suite as oracle_suite
+from tests._inputs import desc_io, make_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def vid(gen, **args):
+    return gen + "".join(f"__{k}-{args[k]}" for k in sorted(args))
+
+
+PAT = dict(dtype="float32", lsize_0=16, lsize_1=16, lid_stride_0=1, lid_stride_1=2048)
+CASES = []
+for k in (1, 2):
+    for E in (32768, 65536 * 3):
+        CASES.append(vid("gmem_pattern", n_input_arrays=k, nelements=E, **PAT))
+    CASES.append(vid("gmem_pattern", n_input_arrays=k, nelements=4096, dtype="float32",
+                     lsize_0=16, lsize_1=16, lid_stride_0=2, lid_stride_1=128))
+    CASES.append(vid("gmem_pattern", n_input_arrays=k, nelements=41472 * 2, dtype="float32",
+                     lsize_0=18, lsize_1=18, lid_stride_0=1, lid_stride_1=2304))
+    CASES.append(vid("gmem_pattern", n_input_arrays=k, nelements=32768, dtype="float64",
+                     lsize_0=16, lsize_1=16, lid_stride_0=1, lid_stride_1=2048))
+for op in ("add", "mul", "madd"):
+    for m in (1, 3):
+        CASES.append(vid(f"flops_{op}_pattern", m=m, nelements=32768, **PAT))
+for m in (0, 1, 5, 16):
+    CASES.append(vid("lmem_shuffle", m=m, nelements=32768, **PAT))
+    CASES.append(vid("overlap_knl", m=m, nelements=32768, **PAT))
+CASES.append(vid("barrier_knl", m=7, nelements=32768, lsize_0=16, lsize_1=16, lid_stride_0=1,
+                 lid_stride_1=2048))
+CASES.append(vid("empty_knl", num_groups=16))
+for dt in ("float32", "float64"):
+    for pf in ("True", "False"):
+        for n in (16, 48, 128):
+            CASES.append(vid("matmul_sq", dtype=dt, prefetch=pf, lsize_0=16, lsize_1=16,
+                             groups_fit="True", n=n))
+            for keep in ("a", "b"):
+                CASES.append(vid("matmul_sq_rm", dtype=dt, prefetch=pf, keep=keep, lsize_0=16,
+                                 lsize_1=16, groups_fit="True", n=n))
+for tile, ns in (("16x16", (14, 28, 112)), ("18x18", (16, 48, 112))):
+    for n in ns:
+        CASES.append(vid("finite_diff", dtype="float32", tile=tile, n=n))
+        for keep in ("u", "res"):
+            CASES.append(vid("finite_diff_rm", dtype="float32", tile=tile, keep=keep, n=n))
+for variant in ("noPF", "uPF", "dmPF", "dmPFtrans"):
+    for nel, np_ in ((32, 16), (48, 64), (16, 128)):
+        CASES.append(vid("dg_diff", dtype="float32", variant=variant, nelements=nel,
+                         nunit_nodes=np_, nmatrices=3))
+        for keep in ("u", "dm", "res"):
+            CASES.append(vid("dg_diff_rm", dtype="float32", variant=variant, keep=keep,
+                             nelements=nel, nunit_nodes=np_, nmatrices=3))
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_1904_09538_b200.device import CudaDevice
+    d = CudaDevice(0)
+    yield d
+    d.close()
+
+
+@pytest.mark.parametrize("mode", ["seed17", "uniform"])
+@pytest.mark.parametrize("variant_id", CASES)
+def test_kernel_matches_oracle_bitwise(dev, variant_id, mode):
+    d, io = desc_io(variant_id)
+    if variant_id.startswith("lmem_shuffle") and d.m == 0:
+        pytest.skip("m=0: the IR stores locbuf_b without ever writing it (undefined value)")
+    ins = make_inputs(d, io, mode, seed=7)
+    got = dev.run(d, ins)
+    want = oracle_suite.run(d, io, ins)
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert g.dtype == w.dtype and g.shape == w.shape
+        np.testing.assert_array_equal(g.view(np.uint8), w.view(np.uint8),
+                                      err_msg=f"{variant_id} ({mode}) differs from the oracle")
+
+
+def test_measure_returns_positive_trials(dev):
+    t = dev.measure(vid("gmem_pattern", n_input_arrays=2, nelements=1 << 22, **PAT), trials=10,
+                    warmup=2)
+    assert len(t) == 10 and all(x > 0 for x in t)
+    mean, kept = dev.measure_summary(vid("empty_knl", num_groups=64), trials=20, warmup=3)
+    assert mean > 0 and 1 <= kept <= 20
+
+
+def test_errors_are_reported_not_silent(dev):
+    from paper_1904_09538_b200 import PsError
+    with pytest.raises(PsError):
+        dev.measure(vid("matmul_sq", dtype="float32", prefetch="True", lsize_0=16, lsize_1=16,
+                        groups_fit="True", n=100), trials=1)
+    with pytest.raises(PsError):
+        dev.measure(vid("empty_knl", num_groups=4), trials=0)
