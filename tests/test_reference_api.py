@@ -1,0 +1,44 @@
+"""The reference's own unit tests and golden generator, compiled from
+/root/reference/proj (read in place) against this repo's C++ host port.
+
+Passing means: the port is a drop-in for the reference API (same types,
+names, error classes) and reproduces its behaviour — every catalog kernel's
+symbolic counts and feature values, the reference interpreter outputs and the
+Levenberg-Marquardt fits are byte-identical to the reference's own output
+(tests/golden/reference.json). Skipped where /root/reference is absent
+(the GPU box)."""
+import os
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+REF = Path("/root/reference/proj")
+pytestmark = pytest.mark.skipif(not REF.is_dir(), reason="reference sources not present")
+
+TESTS = ["test_poly", "test_lang", "test_ir", "test_counting", "test_features", "test_model"]
+
+
+@pytest.fixture(scope="module")
+def built():
+    lib = ROOT / "paper_1904_09538_b200" / "libperfseer_b200.so"
+    if not lib.exists():
+        subprocess.run(["make", "-C", str(ROOT / "paper_1904_09538_b200" / "csrc"), "-j8"], check=True)
+    subprocess.run(["make", "-f", str(ROOT / "tests" / "refapi.mk"), "-j8"], check=True,
+                   capture_output=True)
+    return ROOT / "tests" / "_build"
+
+
+@pytest.mark.parametrize("name", TESTS)
+def test_reference_unit_tests_pass_against_port(built, name):
+    r = subprocess.run([str(built / f"port_{name}")], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "failed: 0" in r.stdout
+
+
+def test_port_reproduces_reference_goldens_byte_for_byte(built):
+    r = subprocess.run([str(built / "port_gen_golden")], capture_output=True, timeout=300)
+    assert r.returncode == 0, r.stderr.decode()
+    golden = (ROOT / "tests" / "golden" / "reference.json").read_bytes()
+    assert r.stdout == golden
