@@ -1,0 +1,515 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 measured-kernel and calibration path.
+
+One step = one pass over the workload's measurement and application kernels
+(BASELINE.json configs[1]: the matmul PF/noPF sweep n = 512..8192 plus the
+B200 microbenchmark sweep that calibrates its model), each kernel launched
+``--trials-per-step`` times and timed with CUDA events on the executor
+stream. Work units (kernel, trial) are LPT-sharded over ranks; after the
+timed region the measurement table is gathered (torch.distributed; NCCL on
+GPUs), rank 0 summarises trials (5x-median filter), computes count features
+with the C++ port, fits the linear and overlap models (Levenberg-Marquardt)
+and predicts the held-out application variants.
+
+metric/unit: suite GB/s = algorithmic global-memory bytes of every launched
+suite kernel / max-over-ranks device time of the timed region; plus the
+model's geomean |pred - meas| / meas per variant. Inputs are resident in HBM
+(filled once; HBM kernels use >= 1 GiB arrays, larger than the 126 MB L2).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def peaks() -> tuple[dict, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured (MEASURED_PEAKS.json)"
+    return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local_rank)
+            dist.init_process_group(backend=backend)
+            self.pg = dist
+            self.backend = backend
+
+    def barrier(self):
+        if self.pg:
+            if self.backend == "nccl":
+                import torch
+                self.pg.barrier(device_ids=[self.local_rank])
+                torch.cuda.synchronize()
+            else:
+                self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        dev = f"cuda:{self.local_rank}" if self.backend == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather_table(self, rows: list[tuple[int, int, float]]) -> list[tuple[int, int, float]]:
+        """All-gather (kernel index, trial index, seconds) records as fixed-size
+        float64 tensors over the process group (NCCL over NVLink on GPUs)."""
+        if not self.pg:
+            return rows
+        import torch
+        dev = f"cuda:{self.local_rank}" if self.backend == "nccl" else "cpu"
+        n = torch.tensor([len(rows)], dtype=torch.int64, device=dev)
+        sizes = [torch.zeros_like(n) for _ in range(self.world)]
+        self.pg.all_gather(sizes, n)
+        cap = int(max(s.item() for s in sizes))
+        buf = torch.full((cap, 3), -1.0, dtype=torch.float64, device=dev)
+        if rows:
+            buf[: len(rows)] = torch.tensor(rows, dtype=torch.float64, device=dev)
+        parts = [torch.empty_like(buf) for _ in range(self.world)]
+        self.pg.all_gather(parts, buf)
+        out = []
+        for p in parts:
+            for k, t, s in p.cpu().tolist():
+                if k >= 0:
+                    out.append((int(k), int(t), s))
+        return out
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+
+class ClockSampler:
+    def __init__(self, device: int):
+        self.device = device
+        self.samples: list[tuple[float, float, int]] = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+
+        def pump():
+            for line in self.proc.stdout:
+                try:
+                    sm, smax, reasons = [x.strip() for x in line.split(",")]
+                    self.samples.append((float(sm), float(smax), int(reasons, 16)))
+                except ValueError:
+                    pass
+
+        self.thread = threading.Thread(target=pump, daemon=True)
+        self.thread.start()
+
+    def stop(self) -> dict:
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        mask = 0
+        for _, _, r in self.samples:
+            mask |= r
+        return {"sm_mhz": statistics.median(s for s, _, _ in self.samples),
+                "sm_max_mhz": max(m for _, m, _ in self.samples),
+                "reasons": [n for b, n in REASONS.items() if mask & b and b != 0x1] or ["none"],
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+
+def workload_kernels(name: str):
+    from paper_1904_09538_b200 import host, workloads
+    wl = workloads.WORKLOADS[name]
+    cal = [k for tags in wl.calibration_tags for k, _ in host.catalog(tags)]
+    app = [k for tags in wl.application_tags for k, _ in host.catalog(tags)]
+    return wl, cal, app
+
+
+def estimate_seconds(io) -> float:
+    return io.bytes_global / 6.0e12 + io.flops / 30e12 + io.bytes_shared / 30e12 + 4e-6
+
+
+def lpt(units: list[tuple[int, int]], est: list[float], world: int) -> list[list[tuple[int, int]]]:
+    """Longest-processing-time-first assignment of (kernel, trial) units."""
+    order = sorted(units, key=lambda u: -est[u[0]])
+    loads = [0.0] * world
+    shards: list[list[tuple[int, int]]] = [[] for _ in range(world)]
+    for u in order:
+        r = min(range(world), key=lambda i: loads[i])
+        shards[r].append(u)
+        loads[r] += est[u[0]]
+    for s in shards:
+        s.sort()
+    return shards
+
+
+def summarize(times: list[float], factor: float = 5.0) -> tuple[float, int]:
+    """executor.cpp:14-38: drop trials > factor x median, mean of the rest."""
+    s = sorted(times)
+    n = len(s)
+    med = s[n // 2] if n % 2 else 0.5 * (s[n // 2 - 1] + s[n // 2])
+    kept = [t for t in times if not t > factor * med]
+    return sum(kept) / len(kept), len(kept)
+
+
+def model_report(wl, cal, app, mean_s: dict[str, float]) -> dict:
+    """Fit every model of the workload on the measured calibration rows and
+    predict the application rows (C++ port: features, LM, predict)."""
+    from paper_1904_09538_b200 import host, workloads
+    out = {}
+    for mname, text in wl.models.items():
+        m = host.HostModel(text)
+        feats = m.feature_table(cal + app)
+        fc, fa = feats[: len(cal)], feats[len(cal):]
+        tc = np.array([mean_s[k] for k in cal])
+        ta = np.array([mean_s[k] for k in app])
+        try:
+            params, stats = m.fit_cpu(fc, tc, scale=True)
+        except Exception as e:  # a fit failure is reported, not hidden
+            out[mname] = {"error": str(e)}
+            continue
+        pred = m.predict_cpu(params, app)
+        per_variant: dict[str, list] = {}
+        for vid, p, t in zip(app, pred, ta):
+            per_variant.setdefault(workloads.variant_of(vid, wl.variant_keys), []).append((p, t))
+        gm = {v: host.geo_mean_rel_error([p for p, _ in pts], [t for _, t in pts])
+              for v, pts in per_variant.items()}
+        # ranking per size: strict '<' first minimum (tools/perfseer.cpp:458-467)
+        by_size: dict[str, list] = {}
+        for vid, p, t in zip(app, pred, ta):
+            by_size.setdefault(workloads.size_of(vid, wl.size_keys), []).append(
+                (workloads.variant_of(vid, wl.variant_keys), p, t))
+        ranks = {}
+        for size, rows in by_size.items():
+            if len(rows) < 2:
+                continue
+            mbest, pbest = rows[0], rows[0]
+            for r in rows:
+                if r[2] < mbest[2]:
+                    mbest = r
+                if r[1] < pbest[1]:
+                    pbest = r
+            ranks[size] = mbest[0] == pbest[0]
+        out[mname] = {
+            "geomean_rel_error": {v: round(x, 5) for v, x in gm.items()},
+            "geomean_rel_error_all": round(host.geo_mean_rel_error(pred, ta), 5),
+            "ranking_correct": f"{sum(ranks.values())}/{len(ranks)}",
+            "fit": {"residual_norm": stats["residual_norm"], "iterations": stats["iterations"],
+                    "converged": stats["converged"]},
+            "params": {n: float(v) for n, v in zip(m.params, params)},
+        }
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle restatement (oracle/suite_ref.c) on host cores
+
+
+def cpu_gmem_sample(elements: int = 1 << 26, reps: int = 3) -> dict:
+    from oracle import suite as oracle_suite
+    from paper_1904_09538_b200 import desc_from_id, kernel_io
+    vid = ("gmem_pattern__dtype-float32__lid_stride_0-1__lid_stride_1-2048__lsize_0-16"
+           f"__lsize_1-16__n_input_arrays-2__nelements-{elements}")
+    d = desc_from_id(vid)
+    io = kernel_io(d)
+    ins = [np.ones(elements, np.float32), np.ones(elements, np.float32)]
+    oracle_suite.run(d, io, ins)  # warm
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle_suite.run(d, io, ins)
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": round(io.bytes_global / dt / 1e9, 2), "unit": "GB/s",
+            "cores": oracle_suite.threads(), "kind": "port",
+            "sample": f"gmem_pattern k=2 restatement (oracle/suite_ref.c, OpenMP) on "
+                      f"E=2^{int(math.log2(elements))} fp32, {reps} reps"}
+
+
+def run_reference_arm(args, dist: Dist) -> None:
+    """bench.py --impl reference: the reference path has no GPU code (SPEC.md:16,
+    597); its CPU implementation of this path is timed on the host cores — the
+    kernel restatement (oracle/suite_ref.c) over a bounded sample of the same
+    workload, plus the reference library's own feature/fit pipeline when
+    oracle/_ref was built."""
+    if dist.rank != 0:
+        return
+    from oracle import suite as oracle_suite
+    from paper_1904_09538_b200 import desc_from_id, kernel_io
+    _, cal, app = workload_kernels(args.workload)
+    sample = []
+    for vid in cal + app:
+        d = desc_from_id(vid)
+        io = kernel_io(d)
+        # bound the sample: skip the cubic-cost kernels above n = 1024 and shrink
+        # HBM arrays to 2^24 elements (still larger than the host LLC)
+        if d.gen in (7, 8) and d.n > 1024:
+            continue
+        if d.gen in (1, 6) and d.nelements > (1 << 24):
+            continue
+        if d.gen == 2 and d.nelements > (1 << 20):
+            continue
+        sample.append((vid, d, io))
+    # add the HBM microbenchmarks at a bounded size
+    for k in (1, 2):
+        vid = ("gmem_pattern__dtype-float32__lid_stride_0-1__lid_stride_1-2048__lsize_0-16"
+               f"__lsize_1-16__n_input_arrays-{k}__nelements-{1 << 24}")
+        d = desc_from_id(vid)
+        sample.append((vid, d, kernel_io(d)))
+    rng = np.random.default_rng(0)
+    inputs = {}
+    for vid, d, io in sample:
+        dt = np.float32 if io.elem_bytes == 4 else np.float64
+        inputs[vid] = [rng.random(io.input_elems[i]).astype(dt) for i in range(io.n_inputs)]
+    for _ in range(args.warmup):
+        for vid, d, io in sample:
+            oracle_suite.run(d, io, inputs[vid])
+    t0 = time.perf_counter()
+    bytes_total = 0.0
+    for _ in range(args.steps):
+        for vid, d, io in sample:
+            oracle_suite.run(d, io, inputs[vid])
+            bytes_total += io.bytes_global
+    dt = time.perf_counter() - t0
+    value = bytes_total / dt / 1e9
+    line = {
+        "impl": "reference", "metric": "suite GB/s", "value": round(value, 3), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: bounded CPU sample ({len(sample)} kernels)"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": oracle_suite.threads(),
+                         "kind": "port",
+                         "sample": f"{len(sample)} suite kernels of the {args.workload} workload "
+                                   "(matmul n<=1024, HBM arrays 2^24) through oracle/suite_ref.c"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def run_ours(args, dist: Dist) -> None:
+    from paper_1904_09538_b200 import desc_from_id, kernel_io
+    from paper_1904_09538_b200.device import CudaDevice, PinnedArray
+
+    wl, cal, app = workload_kernels(args.workload)
+    kernels = cal + app
+    descs = [desc_from_id(k) for k in kernels]
+    ios = [kernel_io(d) for d in descs]
+    est = [estimate_seconds(io) for io in ios]
+    units = [(i, t) for i in range(len(kernels)) for t in range(args.trials_per_step)]
+    mine = lpt(units, est, dist.world)[dist.rank]
+    my_kernels = sorted({i for i, _ in mine})
+
+    dev = CudaDevice(dist.local_rank)
+    for i in my_kernels:  # fill once; inputs stay resident in HBM
+        dev.prepare(descs[i])
+    for _ in range(args.warmup):
+        for i, _t in mine:
+            dev.measure(descs[i], trials=1, warmup=0)
+
+    sampler = ClockSampler(dist.local_rank)
+    sampler.start()
+    time.sleep(0.5)
+    dist.barrier()
+    dev.mark(0)
+    t_wall = time.perf_counter()
+    records: list[tuple[int, int, float]] = []
+    # Consecutive trials of one kernel run back to back (paper methodology,
+    # 60 trials back to back); ps_measure times each launch with events.
+    per_kernel = {}
+    for i, _t in mine:
+        per_kernel[i] = per_kernel.get(i, 0) + 1
+    for step in range(args.steps):
+        for i, cnt in per_kernel.items():
+            for j, s in enumerate(dev.measure(descs[i], trials=cnt, warmup=0)):
+                records.append((i, step * args.trials_per_step + j, s))
+    dev.mark(1)
+    elapsed = dev.elapsed(0, 1)
+    wall = time.perf_counter() - t_wall
+    dist.barrier()
+    clocks = sampler.stop()
+
+    elapsed_max = dist.max(elapsed)
+    table = dist.gather_table(records)
+
+    # e2e through host buffers (ps_run_host: H2D + kernel + D2H per launch)
+    e2e_set = [i for i in my_kernels
+               if not (descs[i].gen in (1, 6) and descs[i].nelements > (1 << 28))]
+    pinned = {}
+    h2d = d2h = 0
+    for i in e2e_set:
+        io = ios[i]
+        ins = [PinnedArray(int(io.input_elems[j]) * io.elem_bytes) for j in range(io.n_inputs)]
+        outs = [PinnedArray(int(io.output_elems[j]) * io.elem_bytes) for j in range(io.n_outputs)]
+        for a in ins:
+            a.numpy(np.uint8)[:] = 0x3f
+        pinned[i] = (ins, outs)
+        h2d += sum(a.nbytes for a in ins)
+        d2h += sum(a.nbytes for a in outs)
+    dev.run_host(descs[e2e_set[0]], *pinned[e2e_set[0]]) if e2e_set else None
+    dist.barrier()
+    e2e_time = 0.0
+    e2e_bytes = 0.0
+    for _ in range(args.steps):
+        for i in e2e_set:
+            e2e_time += dev.run_host(descs[i], *pinned[i])
+            e2e_bytes += ios[i].bytes_global
+    e2e_time_max = dist.max(e2e_time)
+    e2e_bytes_all = e2e_bytes
+    if dist.pg:
+        import torch
+        devn = f"cuda:{dist.local_rank}" if dist.backend == "nccl" else "cpu"
+        t = torch.tensor([e2e_bytes, float(h2d), float(d2h)], dtype=torch.float64, device=devn)
+        dist.pg.all_reduce(t)
+        e2e_bytes_all, h2d, d2h = t.tolist()
+    for ins, outs in pinned.values():
+        for a in ins + outs:
+            a.free()
+
+    if dist.rank != 0:
+        dev.close()
+        return
+
+    # ----- measurement table -> summaries -----
+    trials: dict[int, list[float]] = {}
+    for k, _t, s in table:
+        trials.setdefault(k, []).append(s)
+    mean_s = {}
+    bytes_all = 0.0
+    for k, ts in trials.items():
+        mean_s[kernels[k]] = summarize(ts)[0]
+        bytes_all += ios[k].bytes_global * len(ts)
+    value = bytes_all / elapsed_max / 1e9
+
+    # HBM-class and FLOP-class views of the same timed launches
+    hbm_b = hbm_t = fl = fl_t = 0.0
+    for k, ts in trials.items():
+        if descs[k].gen in (1, 6):
+            hbm_b += ios[k].bytes_global * len(ts)
+            hbm_t += sum(ts)
+        if descs[k].gen in (2, 7):
+            fl += ios[k].flops * len(ts)
+            fl_t += sum(ts)
+
+    # dominant HBM kernel: the largest gmem_pattern launch
+    pk, src = peaks()
+    gm = [k for k in trials if descs[k].gen == 1]
+    dom = max(gm, key=lambda k: ios[k].bytes_global) if gm else None
+    roofline = None
+    if dom is not None:
+        avg = sum(trials[dom]) / len(trials[dom])
+        achieved = ios[dom].bytes_global / avg / 1e9
+        traffic = None
+        tf = ROOT / "profiles" / "ncu_traffic.json"
+        if tf.exists():
+            traffic = json.loads(tf.read_text()).get(kernels[dom])
+        roofline = {"kernel": kernels[dom], "bound": "hbm", "achieved": round(achieved, 1),
+                    "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
+                    "traffic": traffic, "peak_source": src,
+                    "bytes_per_launch": ios[dom].bytes_global}
+
+    models = model_report(wl, cal, app, mean_s)
+    line = {
+        "metric": "suite GB/s", "value": round(value, 3), "unit": "GB/s", "n_gpus": dist.world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(elapsed_max / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (deterministic seed pattern, tests/support.hpp:35-44)",
+        "config": {"workload": wl.description, "kernels": len(kernels),
+                   "calibration_kernels": len(cal), "application_kernels": len(app),
+                   "trials_per_kernel": args.steps * args.trials_per_step,
+                   "l2": "HBM microbenchmarks use >= 1 GiB arrays (> 126 MB L2); no flush",
+                   "parallelism": f"(kernel, trial) units LPT-sharded over {dist.world} rank(s)"},
+        "suite_hbm_GBps": round(hbm_b / hbm_t / 1e9, 1) if hbm_t else None,
+        "suite_flops_TFps": round(fl / fl_t / 1e12, 2) if fl_t else None,
+        "models": models,
+        "roofline": roofline,
+        "cpu_baseline": cpu_gmem_sample() if dist.world == 1 else None,
+        "e2e": {"value": round(e2e_bytes_all / e2e_time_max / 1e9, 3) if e2e_time_max else None,
+                "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "kernels": len(e2e_set), "note": "ps_run_host: pinned host in, H2D + kernel + D2H"},
+        "gpu_launches": int(len(table) + args.steps * len(e2e_set)),
+        "clocks": clocks,
+        "host_wall_s": round(wall, 3),
+    }
+    print(json.dumps(line), flush=True)
+    dev.close()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="matmul")
+    ap.add_argument("--trials-per-step", type=int, default=4)
+    args = ap.parse_args()
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference_arm(args, dist)
+        else:
+            run_ours(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -156,6 +156,18 @@ int ps_run_verify(ps_ctx* ctx, const ps_kernel_desc* desc, const void* const* in
 /* Device pointer of the prepared input/output i (for zero-copy callers). */
 int ps_buffer(ps_ctx* ctx, int is_output, int index, void** dev_ptr, int64_t* elems);
 
+/* End to end through host buffers: H2D of every input, one launch, D2H of
+ * every output, bracketed by CUDA events; seconds = the whole sequence. */
+int ps_run_host(ps_ctx* ctx, const ps_kernel_desc* desc, const void* const* inputs, int n_inputs,
+                void* const* outputs, int n_outputs, double* seconds);
+/* Pinned host memory for ps_run_host callers. */
+int ps_host_alloc(size_t bytes, void** ptr);
+int ps_host_free(void* ptr);
+
+/* Event markers on the context stream (slots 0..63) for timing whole steps. */
+int ps_mark(ps_ctx* ctx, int slot);
+int ps_elapsed(ps_ctx* ctx, int from_slot, int to_slot, double* seconds);
+
 /* --- calibration (K17) and prediction (K18) ------------------------------ */
 
 /* Compiled model expression: postfix bytecode over params/features/constants
@@ -224,6 +236,38 @@ typedef struct ps_variant_tables {
 
 int ps_eval_batched(ps_ctx* ctx, const ps_variant_tables* tables, const int64_t* points,
                     int64_t npts, double* pred, uint8_t* argmin);
+
+/* --- host pipeline over the C++ port (no GPU) ----------------------------
+ * Text in, caller-owned buffers out. Lists are newline-separated. */
+
+/* KernelCollection::generate (uipick.cpp:71-119) over catalog "reference"
+ * (builtin_generators, uipick.cpp:669-804) or "b200" (B200 ladders + DG);
+ * tags one per line, match = identical|subset|superset|intersect. Output:
+ * "variant_id\tbindings\n" per kernel. */
+int ps_catalog(const char* catalog, const char* tags, const char* match, char* out, size_t cap,
+               size_t* needed);
+/* parse_model_file (model.cpp:625-644) -> JSON {output, expression, params,
+ * features, cost_params}. */
+int ps_model_info(const char* model_text, char* out, size_t cap, size_t* needed);
+/* gather_feature_values (features.cpp:473-493) for the model's features over
+ * kernels given by variant id: out[k * nf + f]. */
+int ps_feature_table(const char* model_text, const char* variant_ids, int sub_group_size,
+                     double* out, int64_t cap_values);
+/* fit_model (model.cpp:485-606), bit-identical to the reference; scale != 0
+ * applies scale_features_by_output (model.cpp:421-435) first. */
+int ps_fit_cpu(const char* model_text, const double* features, const double* t, int nr, int scale,
+               const ps_fit_opts* opts, double* params_out, ps_fit_stats* stats);
+/* The reference's deterministic LM start (model.cpp:439-481). */
+int ps_initial_point(const char* model_text, const double* features, const double* t, int nr,
+                     int scale, double* params_out);
+/* predict (model.cpp:615-623) per kernel variant id. */
+int ps_predict_cpu(const char* model_text, const double* params, const char* variant_ids,
+                   int sub_group_size, double* out, int64_t cap);
+/* Postfix bytecode of the model (which = -1) or of d model / d p_which. */
+int ps_model_bytecode(const char* model_text, int which, int32_t* ops, int cap_ops, double* consts,
+                      int cap_consts, int* n_ops, int* n_consts, int* max_stack);
+/* geo_mean_rel_error (executor.cpp:50-61). */
+int ps_geo_mean_rel_error(const double* pred, const double* meas, int n, double* out);
 
 #ifdef __cplusplus
 }

@@ -102,6 +102,14 @@ def _declare(L: C.CDLL) -> None:
     L.ps_fit_lm_batched.argtypes = [C.c_void_p, P(Bytecode), P(Bytecode), C.c_int, C.c_int,
                                     P(C.c_double), P(C.c_double), C.c_int, C.c_int,
                                     P(FitOpts), P(C.c_double), P(FitStats)]
+    L.ps_run_host.argtypes = [C.c_void_p, P(KernelDesc), P(C.c_void_p), C.c_int, P(C.c_void_p),
+                              C.c_int, P(C.c_double)]
+    L.ps_host_alloc.argtypes = [C.c_size_t, P(C.c_void_p)]
+    L.ps_host_free.argtypes = [C.c_void_p]
+    L.ps_mark.argtypes = [C.c_void_p, C.c_int]
+    L.ps_elapsed.argtypes = [C.c_void_p, C.c_int, C.c_int, P(C.c_double)]
+    for name in ("ps_run_host", "ps_host_alloc", "ps_host_free", "ps_mark", "ps_elapsed"):
+        getattr(L, name).restype = C.c_int
     for name in ("ps_desc_from_id", "ps_kernel_io", "ps_init", "ps_destroy", "ps_device_info",
                  "ps_prepare", "ps_measure", "ps_measure_summary", "ps_run_timed",
                  "ps_run_verify", "ps_buffer", "ps_fit_lm_batched", "ps_eval_batched"):

@@ -414,34 +414,81 @@ int Ctx::ensure(DevBuf& b, size_t bytes) {
   return PS_OK;
 }
 
+void Ctx::activate(Slot& s) {
+  for (int i = 0; i < PS_MAX_ARRAYS; ++i) {
+    in[i].ptr = s.in[i].ptr;
+    out[i].ptr = s.out[i].ptr;
+  }
+  io = s.io;
+  s.last_use = ++tick;
+}
+
+void Ctx::release(Slot& s) {
+  for (auto* bufs : {s.in, s.out})
+    for (int i = 0; i < PS_MAX_ARRAYS; ++i)
+      if (bufs[i].ptr) {
+        cudaFree(bufs[i].ptr);
+        bufs[i].ptr = nullptr;
+        bufs[i].cap = 0;
+      }
+  cache_bytes -= std::min(cache_bytes, s.bytes);
+  s.bytes = 0;
+}
+
 int prepare(Ctx* c, const ps_kernel_desc* d, int fill_mode, uint64_t seed) {
   PS_CUDA(cudaSetDevice(c->device));
   ps_io_info io;
   int rc = kernel_io(d, &io);
   if (rc) return rc;
-  bool same = c->prepared && std::memcmp(&c->desc, d, sizeof *d) == 0 &&
-              c->fill_mode == fill_mode && c->seed == seed;
-  if (same) return PS_OK;
+  const std::string key(reinterpret_cast<const char*>(d), sizeof *d);
+  auto hit = c->slots.find(key);
+  if (hit != c->slots.end() && hit->second.fill_mode == fill_mode && hit->second.seed == seed) {
+    c->activate(hit->second);
+    c->desc = *d;
+    c->prepared = true;
+    return PS_OK;
+  }
+  size_t need = 0;
+  for (int i = 0; i < io.n_inputs; ++i) need += (size_t)io.input_elems[i] * io.elem_bytes;
+  for (int i = 0; i < io.n_outputs; ++i) need += (size_t)io.output_elems[i] * io.elem_bytes;
+  if (hit != c->slots.end()) {
+    c->release(hit->second);
+    c->slots.erase(hit);
+  }
+  // Evict least-recently-used variants until the new one fits the budget.
+  while (c->cache_bytes + need > c->cache_cap && !c->slots.empty()) {
+    auto lru = c->slots.begin();
+    for (auto it = c->slots.begin(); it != c->slots.end(); ++it)
+      if (it->second.last_use < lru->second.last_use) lru = it;
+    c->release(lru->second);
+    c->slots.erase(lru);
+  }
+  Slot& s = c->slots[key];
+  s.io = io;
+  s.fill_mode = fill_mode;
+  s.seed = seed;
+  s.bytes = need;
+  c->cache_bytes += need;
   for (int i = 0; i < io.n_inputs; ++i) {
     size_t bytes = (size_t)io.input_elems[i] * io.elem_bytes;
-    if ((rc = c->ensure(c->in[i], bytes))) return rc;
+    if ((rc = c->ensure(s.in[i], bytes))) return rc;
     uint64_t h = fnv1a_name(input_name(d, i));
     int blocks = (int)std::min<int64_t>((io.input_elems[i] + 255) / 256, c->sm_count * 32);
     if (fill_mode == PS_FILL_SEED17)
-      fill_seed17<<<blocks, 256, 0, c->stream>>>(c->in[i].ptr, io.input_elems[i], io.elem_bytes, h);
+      fill_seed17<<<blocks, 256, 0, c->stream>>>(s.in[i].ptr, io.input_elems[i], io.elem_bytes, h);
     else
-      fill_uniform<<<blocks, 256, 0, c->stream>>>(c->in[i].ptr, io.input_elems[i], io.elem_bytes,
+      fill_uniform<<<blocks, 256, 0, c->stream>>>(s.in[i].ptr, io.input_elems[i], io.elem_bytes,
                                                   h ^ (seed * 0x9e3779b97f4a7c15ull));
     PS_CUDA(cudaGetLastError());
   }
   for (int i = 0; i < io.n_outputs; ++i) {
     size_t bytes = (size_t)io.output_elems[i] * io.elem_bytes;
-    if ((rc = c->ensure(c->out[i], bytes))) return rc;
-    PS_CUDA(cudaMemsetAsync(c->out[i].ptr, 0, bytes, c->stream));
+    if ((rc = c->ensure(s.out[i], bytes))) return rc;
+    PS_CUDA(cudaMemsetAsync(s.out[i].ptr, 0, bytes, c->stream));
   }
   PS_CUDA(cudaStreamSynchronize(c->stream));
+  c->activate(s);
   c->desc = *d;
-  c->io = io;
   c->fill_mode = fill_mode;
   c->seed = seed;
   c->prepared = true;
@@ -679,6 +726,12 @@ int ps_init(int device, ps_ctx** out) {
                      device, prop.major, prop.minor);
   }
   PS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  {
+    size_t fr = 0, tot = 0;
+    PS_CUDA(cudaMemGetInfo(&fr, &tot));
+    c->cache_cap = (size_t)((double)fr * 0.7);  // resident-variant budget (HBM)
+    if (const char* cap = getenv("PS_CACHE_GB")) c->cache_cap = (size_t)(atof(cap) * 1e9);
+  }
   const char* gen = getenv("PS_GMEM_GENERIC");
   c->force_generic = gen && gen[0] == '1';
   *out = reinterpret_cast<ps_ctx*>(c);
@@ -690,13 +743,12 @@ int ps_destroy(ps_ctx* ctx) {
   if (!c) return PS_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  for (auto& b : c->in)
-    if (b.ptr) cudaFree(b.ptr);
-  for (auto& b : c->out)
-    if (b.ptr) cudaFree(b.ptr);
+  for (auto& kv : c->slots) c->release(kv.second);
+  c->release(c->host_slot);
   for (auto& b : c->scratch)
     if (b.ptr) cudaFree(b.ptr);
   for (auto e : c->ev) cudaEventDestroy(e);
+  for (auto e : c->marks) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
   delete c;
   return PS_OK;
@@ -808,17 +860,20 @@ int ps_run_verify(ps_ctx* ctx, const ps_kernel_desc* desc, const void* const* in
     return set_error(PS_ERR_ARG, "kernel takes %d inputs / %d outputs, got %d / %d",
                      io.n_inputs, io.n_outputs, n_inputs, n_outputs);
   PS_CUDA(cudaSetDevice(c->device));
+  Slot& hs = c->host_slot;
   for (int i = 0; i < io.n_inputs; ++i) {
     size_t bytes = (size_t)io.input_elems[i] * io.elem_bytes;
-    if ((rc = c->ensure(c->in[i], bytes))) return rc;
-    PS_CUDA(cudaMemcpyAsync(c->in[i].ptr, inputs[i], bytes, cudaMemcpyHostToDevice, c->stream));
+    if ((rc = c->ensure(hs.in[i], bytes))) return rc;
+    PS_CUDA(cudaMemcpyAsync(hs.in[i].ptr, inputs[i], bytes, cudaMemcpyHostToDevice, c->stream));
   }
   for (int i = 0; i < io.n_outputs; ++i) {
     size_t bytes = (size_t)io.output_elems[i] * io.elem_bytes;
-    if ((rc = c->ensure(c->out[i], bytes))) return rc;
-    PS_CUDA(cudaMemsetAsync(c->out[i].ptr, 0, bytes, c->stream));
+    if ((rc = c->ensure(hs.out[i], bytes))) return rc;
+    PS_CUDA(cudaMemsetAsync(hs.out[i].ptr, 0, bytes, c->stream));
   }
-  c->prepared = false;  // buffers now hold caller data
+  hs.io = io;
+  c->activate(hs);
+  c->prepared = false;  // active buffers hold caller data
   if ((rc = launch(c, desc))) return rc;
   for (int i = 0; i < io.n_outputs; ++i) {
     size_t bytes = (size_t)io.output_elems[i] * io.elem_bytes;
@@ -836,6 +891,86 @@ int ps_buffer(ps_ctx* ctx, int is_output, int index, void** dev_ptr, int64_t* el
   if (index < 0 || index >= n) return set_error(PS_ERR_ARG, "ps_buffer: index out of range");
   *dev_ptr = is_output ? c->out[index].ptr : c->in[index].ptr;
   if (elems) *elems = is_output ? c->io.output_elems[index] : c->io.input_elems[index];
+  return PS_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Step markers and end-to-end runs (bench timing on the context stream).
+
+extern "C" {
+
+int ps_mark(ps_ctx* ctx, int slot) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || slot < 0 || slot >= 64) return set_error(PS_ERR_ARG, "ps_mark: bad argument");
+  PS_CUDA(cudaSetDevice(c->device));
+  while ((int)c->marks.size() <= slot) {
+    cudaEvent_t e;
+    PS_CUDA(cudaEventCreate(&e));
+    c->marks.push_back(e);
+  }
+  PS_CUDA(cudaEventRecord(c->marks[slot], c->stream));
+  return PS_OK;
+}
+
+int ps_elapsed(ps_ctx* ctx, int from, int to, double* seconds) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !seconds || from < 0 || to < 0 || from >= (int)c->marks.size() ||
+      to >= (int)c->marks.size())
+    return set_error(PS_ERR_ARG, "ps_elapsed: bad argument");
+  PS_CUDA(cudaEventSynchronize(c->marks[to]));
+  float ms = 0.f;
+  PS_CUDA(cudaEventElapsedTime(&ms, c->marks[from], c->marks[to]));
+  *seconds = (double)ms * 1e-3;
+  return PS_OK;
+}
+
+int ps_run_host(ps_ctx* ctx, const ps_kernel_desc* desc, const void* const* inputs, int n_inputs,
+                void* const* outputs, int n_outputs, double* seconds) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !desc || !seconds) return set_error(PS_ERR_ARG, "ps_run_host: null argument");
+  int rc = validate_desc(desc);
+  if (rc) return rc;
+  ps_io_info io;
+  if ((rc = kernel_io(desc, &io))) return rc;
+  if (n_inputs != io.n_inputs || n_outputs != io.n_outputs)
+    return set_error(PS_ERR_ARG, "kernel takes %d inputs / %d outputs, got %d / %d", io.n_inputs,
+                     io.n_outputs, n_inputs, n_outputs);
+  PS_CUDA(cudaSetDevice(c->device));
+  Slot& hs = c->host_slot;
+  for (int i = 0; i < io.n_inputs; ++i)
+    if ((rc = c->ensure(hs.in[i], (size_t)io.input_elems[i] * io.elem_bytes))) return rc;
+  for (int i = 0; i < io.n_outputs; ++i)
+    if ((rc = c->ensure(hs.out[i], (size_t)io.output_elems[i] * io.elem_bytes))) return rc;
+  if ((rc = events(c, 2))) return rc;
+  hs.io = io;
+  c->activate(hs);
+  c->prepared = false;
+  PS_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  for (int i = 0; i < io.n_inputs; ++i)
+    PS_CUDA(cudaMemcpyAsync(c->in[i].ptr, inputs[i], (size_t)io.input_elems[i] * io.elem_bytes,
+                            cudaMemcpyHostToDevice, c->stream));
+  if ((rc = launch(c, desc))) return rc;
+  for (int i = 0; i < io.n_outputs; ++i)
+    PS_CUDA(cudaMemcpyAsync(outputs[i], c->out[i].ptr, (size_t)io.output_elems[i] * io.elem_bytes,
+                            cudaMemcpyDeviceToHost, c->stream));
+  PS_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  PS_CUDA(cudaEventSynchronize(c->ev[1]));
+  float ms = 0.f;
+  PS_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  *seconds = (double)ms * 1e-3;
+  return PS_OK;
+}
+
+int ps_host_alloc(size_t bytes, void** ptr) {
+  if (!ptr) return set_error(PS_ERR_ARG, "ps_host_alloc: null out");
+  PS_CUDA(cudaHostAlloc(ptr, bytes, cudaHostAllocDefault));
+  return PS_OK;
+}
+
+int ps_host_free(void* ptr) {
+  if (ptr) PS_CUDA(cudaFreeHost(ptr));
   return PS_OK;
 }
 

@@ -6,6 +6,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <map>
+#include <string>
 #include <vector>
 
 #include "../../../include/perfseer_b200.h"
@@ -17,6 +19,18 @@ struct DevBuf {
   size_t cap = 0;
 };
 
+// Device arrays of one prepared kernel variant. Slots stay resident (inputs
+// filled once, in HBM) until the LRU cache exceeds its byte budget.
+struct Slot {
+  DevBuf in[PS_MAX_ARRAYS];
+  DevBuf out[PS_MAX_ARRAYS];
+  ps_io_info io{};
+  int fill_mode = -1;
+  uint64_t seed = 0;
+  uint64_t last_use = 0;
+  size_t bytes = 0;
+};
+
 struct Ctx {
   int device = 0;
   int sm_count = 0;
@@ -24,9 +38,14 @@ struct Ctx {
   size_t l2_bytes = 0;
   cudaStream_t stream = nullptr;
   std::vector<cudaEvent_t> ev;
-  DevBuf in[PS_MAX_ARRAYS];
+  std::vector<cudaEvent_t> marks;  // ps_mark slots
+  DevBuf in[PS_MAX_ARRAYS];   // views of the active slot (not owned)
   DevBuf out[PS_MAX_ARRAYS];
   DevBuf scratch[8];
+  std::map<std::string, Slot> slots;  // keyed by the raw descriptor bytes
+  Slot host_slot;                     // caller-data runs (verify / run_host)
+  size_t cache_bytes = 0, cache_cap = 0;
+  uint64_t tick = 0;
   bool prepared = false;
   ps_kernel_desc desc{};
   ps_io_info io{};
@@ -38,6 +57,8 @@ struct Ctx {
   float flop_step = 0.015625f;
 
   int ensure(DevBuf& b, size_t bytes);
+  void activate(Slot& s);
+  void release(Slot& s);
 };
 
 int set_error(int code, const char* fmt, ...);

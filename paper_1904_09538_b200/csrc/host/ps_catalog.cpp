@@ -738,7 +738,7 @@ std::vector<Generator> b200_generators() {
   {
     VArgs v{{"dtype", {"float32"}}, {"nelements", hbm}, {"lsize_0", {"16"}}, {"lsize_1", {"16"}},
             {"lid_stride_0", {"1"}}, {"lid_stride_1", {"2048"}}, {"n_input_arrays", {"1", "2"}}};
-    out.push_back(gen("gmem_pattern", v, make_gmem_pattern));
+    out.push_back(gen("gmem_pattern", v, make_gmem_pattern, {"gmem_pattern", "gmem_pattern_16"}));
     // 18x18 work-groups, gid(0) stride 18.
     VArgs v18{{"dtype", {"float32"}}, {"nelements", {"268406784", "402610176", "536813568", "671016960"}},
               {"lsize_0", {"18"}}, {"lsize_1", {"18"}}, {"lid_stride_0", {"1"}}, {"lid_stride_1", {"2304"}},

@@ -96,3 +96,48 @@ class CudaDevice:
         out_ptrs = (C.c_void_p * max(1, len(outs)))(*[a.ctypes.data for a in outs])
         check(lib().ps_run_verify(self._ctx, C.byref(d), in_ptrs, len(ins), out_ptrs, len(outs)))
         return outs
+
+    # -- timing helpers (events on the context stream) ---------------------
+    def mark(self, slot: int) -> None:
+        check(lib().ps_mark(self._ctx, slot))
+
+    def elapsed(self, a: int, b: int) -> float:
+        s = C.c_double()
+        check(lib().ps_elapsed(self._ctx, a, b, C.byref(s)))
+        return s.value
+
+    def run_host(self, kernel, inputs: list["PinnedArray"], outputs: list["PinnedArray"]) -> float:
+        """H2D + launch + D2H through caller-owned (pinned) host buffers; seconds."""
+        d = _desc(kernel)
+        ip = (C.c_void_p * max(1, len(inputs)))(*[a.ptr for a in inputs])
+        op = (C.c_void_p * max(1, len(outputs)))(*[a.ptr for a in outputs])
+        s = C.c_double()
+        check(lib().ps_run_host(self._ctx, C.byref(d), ip, len(inputs), op, len(outputs),
+                                C.byref(s)))
+        return s.value
+
+
+class PinnedArray:
+    """Page-locked host buffer from ps_host_alloc, viewable as numpy."""
+
+    def __init__(self, nbytes: int):
+        self.nbytes = nbytes
+        p = C.c_void_p()
+        check(lib().ps_host_alloc(nbytes, C.byref(p)))
+        self.ptr = p.value
+
+    def numpy(self, dtype) -> np.ndarray:
+        n = self.nbytes // np.dtype(dtype).itemsize
+        buf = (C.c_char * self.nbytes).from_address(self.ptr)
+        return np.frombuffer(buf, dtype=dtype, count=n)
+
+    def free(self) -> None:
+        if self.ptr:
+            lib().ps_host_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

@@ -1,0 +1,114 @@
+"""Calibration workloads: which measurement kernels calibrate which model, and
+which application variants the calibrated model must predict.
+
+Each workload follows the paper's Fig. 5 pairing of models, measurement
+kernels and features and SURVEY Appendix C's model
+expressions in the reference grammar; kernels come from the B200 catalog
+(ps_catalog "b200", csrc/host/ps_catalog.cpp).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+OUTPUT = "f_exec_wall_time_cuda_b200_0"
+
+# Feature ids (reference grammar, features.cpp:124-249).
+G16 = "f_mem_access_global_float32_lstrides:{0:1;1:>1}_gstrides:{0:16;1:>16}_afr:1"
+OPS = {"add": "f_op_float32_add", "mul": "f_op_float32_mul", "madd": "f_op_float32_madd"}
+LMEM = "f_mem_access_local_float32"
+BAR = "f_sync_barrier_local"
+GROUPS = "f_thread_groups"
+LAUNCH = "f_sync_kernel_launch"
+
+
+def _tag(t: str) -> str:
+    return f"f_mem_access_tag:{t}"
+
+
+def _sum(terms: list[str]) -> str:
+    return " + ".join(terms)
+
+
+def linear_model(gmem: list[tuple[str, str]], onchip: list[tuple[str, str]]) -> str:
+    """ovh + c_gmem + c_onchip (paper Eq. 1)."""
+    ovh = [f"p_bar * {BAR} * {GROUPS}", f"p_group * {GROUPS}", f"p_launch * {LAUNCH}"]
+    terms = ovh + [f"{p} * {f}" for p, f in gmem] + [f"{p} * {f}" for p, f in onchip]
+    return OUTPUT + "\n" + _sum(terms) + "\n"
+
+
+def overlap_model(gmem: list[tuple[str, str]], onchip: list[tuple[str, str]]) -> str:
+    """ovh + cg*sstep(cg - co; p_edge) + co*sstep(co - cg; p_edge) (Eqs. 4-5)."""
+    ovh = _sum([f"p_bar * {BAR} * {GROUPS}", f"p_group * {GROUPS}", f"p_launch * {LAUNCH}"])
+    cg = "(" + _sum([f"{p} * {f}" for p, f in gmem]) + ")"
+    co = "(" + _sum([f"{p} * {f}" for p, f in onchip]) + ")"
+    return (OUTPUT + "\n" + ovh + f" + {cg} * sstep({cg} - {co}; p_edge) + "
+            f"{co} * sstep({co} - {cg}; p_edge)\n")
+
+
+ONCHIP = [("p_f32add", OPS["add"]), ("p_f32mul", OPS["mul"]), ("p_f32madd", OPS["madd"]),
+          ("p_f32l", LMEM)]
+
+# Microbenchmark tag sets common to every application (ps_catalog "b200").
+MICRO_TAGS = [
+    ["gmem_pattern_16"],
+    ["flops_add_pattern"], ["flops_mul_pattern"], ["flops_madd_pattern"],
+    ["lmem_shuffle"], ["barrier_knl"], ["empty_knl"], ["overlap_knl"],
+]
+
+
+@dataclass
+class Workload:
+    name: str
+    description: str
+    calibration_tags: list[list[str]]
+    application_tags: list[list[str]]
+    models: dict[str, str]
+    # variant identity for per-variant error: generator args except the size
+    variant_keys: tuple[str, ...] = ("prefetch",)
+    size_keys: tuple[str, ...] = ("n",)
+    hbm_generators: tuple[str, ...] = ("gmem_pattern", "overlap_knl")
+    extra: dict = field(default_factory=dict)
+
+
+MATMUL_GMEM = [("p_g16", G16), ("p_mmPFa", _tag("mm-PF-a")), ("p_mmPFb", _tag("mm-PF-b")),
+               ("p_mmnoPFa", _tag("mm-noPF-a")), ("p_mmnoPFb", _tag("mm-noPF-b"))]
+
+MATMUL = Workload(
+    name="matmul",
+    description=("BASELINE.json configs[1]: square fp32 matmul, prefetch (PF) and no-prefetch "
+                 "(noPF) 16x16 variants, n = 512..8192, model calibrated on B200 from the "
+                 "microbenchmark sweep plus the mm-* work-removed kernels (PAPER.md:2145-2330)"),
+    calibration_tags=MICRO_TAGS + [["matmul_sq_rm"]],
+    application_tags=[["matmul_sq"]],
+    models={"linear": linear_model(MATMUL_GMEM, ONCHIP),
+            "nonlinear": overlap_model(MATMUL_GMEM, ONCHIP)},
+    variant_keys=("prefetch",),
+    size_keys=("n",),
+)
+
+FD_GMEM = [("p_g16", G16), ("p_fd16u", _tag("fd-16x16-u")), ("p_fd16res", _tag("fd-16x16-res"))]
+
+FD = Workload(
+    name="fd",
+    description=("BASELINE.json configs[0]: five-point FD stencil, 16x16 tiles, grids "
+                 "1120^2..8176^2, linear model (PAPER.md:2560-2670)"),
+    calibration_tags=MICRO_TAGS + [["finite_diff_rm", "tile:16x16"]],
+    application_tags=[["finite_diff", "tile:16x16"]],
+    models={"linear": linear_model(FD_GMEM, ONCHIP)},
+    variant_keys=("tile",),
+    size_keys=("n",),
+)
+
+WORKLOADS = {w.name: w for w in (MATMUL, FD)}
+
+
+def variant_of(variant_id: str, keys: tuple[str, ...]) -> str:
+    gen, *parts = variant_id.split("__")
+    args = dict(p.split("-", 1) for p in parts)
+    return gen + "".join(f"_{k}-{args[k]}" for k in keys if k in args)
+
+
+def size_of(variant_id: str, keys: tuple[str, ...]) -> str:
+    _, *parts = variant_id.split("__")
+    args = dict(p.split("-", 1) for p in parts)
+    return ";".join(f"{k}={args[k]}" for k in keys if k in args)
