@@ -208,6 +208,13 @@ typedef struct ps_fit_stats {
 int ps_fit_lm_batched(ps_ctx* ctx, const ps_bytecode* model, const ps_bytecode* jac, int np,
                       int nf, const double* features, const double* t, int nr, int nbatch,
                       const ps_fit_opts* opts, double* params_inout, ps_fit_stats* stats);
+/* Same with mode bits: 1 = column equilibration (iterate on q = p / |p0|),
+ * 2 = warp-shuffle reductions (default: per-entry sums in the reference's
+ * row order, which makes linear fits bit-identical to fit_model). */
+int ps_fit_lm_batched_ex(ps_ctx* ctx, const ps_bytecode* model, const ps_bytecode* jac, int np,
+                         int nf, const double* features, const double* t, int nr, int nbatch,
+                         const ps_fit_opts* opts, int mode, double* params_inout,
+                         ps_fit_stats* stats);
 
 /* Batched prediction over a variant space. Each of the nvar variants carries
  * a count table: nf features, each an exact polynomial in the point's

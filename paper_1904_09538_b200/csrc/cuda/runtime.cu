@@ -582,6 +582,15 @@ int launch(Ctx* c, const ps_kernel_desc* d) {
       break;
     case PS_GEN_OVERLAP: {
       Pattern p = make_pattern(d);
+      if (p.s0 == 1 && d->nelements % 4 == 0 && !c->force_generic) {
+        constexpr int ROWS = 4;
+        const int64_t vecs = d->nelements / 4;
+        int64_t blocks = (vecs + 256 * ROWS - 1) / (256 * ROWS);
+        blocks = std::min<int64_t>(blocks, (int64_t)c->sm_count * 8);
+        overlap_rows<ROWS><<<(unsigned)blocks, 256, 0, st>>>((const float*)in0, (float*)out0, vecs,
+                                                            (int)d->m);
+        break;
+      }
       dim3 block(p.L0, p.L1);
       size_t sm = 2 * sizeof(float) * p.L0 * p.L1;
       overlap_knl<<<(unsigned)(p.G0 * p.G1), block, sm, st>>>((const float*)in0, (float*)out0, p,

@@ -193,6 +193,52 @@ __global__ void __launch_bounds__(1024) overlap_knl(const float* __restrict__ in
   out[g] = tmp;
 }
 
+// K8 overlap_knl, contiguous layout (s0 = 1): the same coarsening as
+// gmem_pattern_rows — a thread executes 4 consecutive lx work-items (one
+// 16-byte vector) of ROWS work-group rows. Per work-item the IR order is
+// kept: global load, m shared load/store pairs on the work-item's own
+// locbuf slot (vectorised 16-byte LDS/STS over the thread's 4 work-items),
+// global store. The ROWS global loads are issued before the shared work, so
+// HBM latency overlaps the on-chip traffic exactly as the kernel intends.
+template <int ROWS>
+__global__ void __launch_bounds__(256) overlap_rows(const float* __restrict__ in0,
+                                                   float* __restrict__ out, int64_t total_vecs,
+                                                   int m) {
+  __shared__ float4 sa[256], sb[256];
+  const float4* a = reinterpret_cast<const float4*>(in0);
+  float4* o = reinterpret_cast<float4*>(out);
+  const unsigned pa = static_cast<unsigned>(__cvta_generic_to_shared(&sa[threadIdx.x]));
+  const unsigned pb = static_cast<unsigned>(__cvta_generic_to_shared(&sb[threadIdx.x]));
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * ROWS;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x * ROWS + threadIdx.x; base < total_vecs;
+       base += stride) {
+    float4 v[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const int64_t i = base + (int64_t)r * blockDim.x;
+      if (i < total_vecs) v[r] = __ldcs(a + i);
+    }
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      for (int t = 0; t < m; ++t) {
+        float x, y, z, w;
+        asm volatile("ld.volatile.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(x), "=f"(y), "=f"(z), "=f"(w)
+                     : "r"(pa)
+                     : "memory");
+        asm volatile("st.volatile.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(pb), "f"(x), "f"(y),
+                     "f"(z), "f"(w)
+                     : "memory");
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const int64_t i = base + (int64_t)r * blockDim.x;
+      if (i < total_vecs) __stcs(o + i, v[r]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K9 matmul_sq noPF (uipick.cpp:478-502): c[i,j] = sum_k a[i,k]*b[k,j] with
 // i = 16*i_out + i_in (g.1, l.1), j = 16*j_out + j_in (g.0, l.0); one madd

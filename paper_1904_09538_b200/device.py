@@ -141,3 +141,51 @@ class PinnedArray:
             self.free()
         except Exception:
             pass
+
+
+def fit_lm_batched(dev: CudaDevice, model, features: np.ndarray, t: np.ndarray, p0: np.ndarray,
+                   opts=None, mode: int = 0):
+    """K17 on `dev`: nbatch independent LM fits of a HostModel.
+
+    features: [nbatch, nr, nf] (or [nr, nf], shared by every start), t: [nbatch, nr]
+    or [nr], p0: [nbatch, np]. Returns (params [nbatch, np], stats list)."""
+    from ._abi import Bytecode, FitOpts, FitStats
+    from .host import default_fit_opts
+    L = lib()
+    if not getattr(L, "_lm_declared", False):
+        L.ps_fit_lm_batched_ex.argtypes = [C.c_void_p, C.POINTER(Bytecode), C.POINTER(Bytecode),
+                                           C.c_int, C.c_int, C.POINTER(C.c_double),
+                                           C.POINTER(C.c_double), C.c_int, C.c_int,
+                                           C.POINTER(FitOpts), C.c_int, C.POINTER(C.c_double),
+                                           C.POINTER(FitStats)]
+        L.ps_fit_lm_batched_ex.restype = C.c_int
+        L._lm_declared = True
+    p0 = np.atleast_2d(np.asarray(p0, dtype=np.float64))
+    nb, npar = p0.shape
+    f = np.asarray(features, dtype=np.float64)
+    if f.ndim == 2:
+        f = np.broadcast_to(f, (nb,) + f.shape)
+    tt = np.asarray(t, dtype=np.float64)
+    if tt.ndim == 1:
+        tt = np.broadcast_to(tt, (nb, tt.shape[0]))
+    f = np.ascontiguousarray(f)
+    tt = np.ascontiguousarray(tt)
+    nr, nf = f.shape[1], f.shape[2]
+    keep = []
+
+    def bc(which):
+        ops, consts, _ = model.bytecode(which)
+        keep.extend([ops, consts])
+        return Bytecode(len(ops), len(consts), ops.ctypes.data_as(C.POINTER(C.c_int32)),
+                        consts.ctypes.data_as(C.POINTER(C.c_double)))
+
+    mb = bc(-1)
+    jac = (Bytecode * npar)(*[bc(i) for i in range(npar)])
+    params = np.ascontiguousarray(p0.copy())
+    stats = (FitStats * nb)()
+    o = opts or default_fit_opts()
+    dptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    check(L.ps_fit_lm_batched_ex(dev._ctx, C.byref(mb), jac, npar, nf, dptr(f), dptr(tt), nr, nb,
+                                 C.byref(o), mode, dptr(params), stats))
+    return params, [{"residual_norm": s.residual_norm, "iterations": s.iterations,
+                     "converged": bool(s.converged), "status": s.status} for s in stats]
