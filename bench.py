@@ -260,13 +260,13 @@ def model_report(wl, cal, app, mean_s: dict[str, float], dev=None) -> dict:
             fs, ts = fc / tc[:, None], np.ones_like(tc)
             p0 = m.initial_point(fc, tc, scale=True)
             starts = [p0]
-            if "p_edge" in m.params:
-                ie = m.params.index("p_edge")
+            edges = [i for i, c in enumerate(m.cost_params) if not c]  # tanh-only params
+            if edges:
                 for e in (3.0, 10.0, 30.0, 100.0, 300.0, 1000.0):
                     s = p0.copy()
-                    s[ie] = e
+                    s[edges] = e
                     starts.append(s)
-            starts = np.abs(np.stack(starts))  # cost parameters start non-negative
+            starts = np.stack(starts)
             t0 = time.perf_counter()
             params, stats = fit_lm_batched(dev, m, fs, ts, starts, mode=1)
             dt = time.perf_counter() - t0

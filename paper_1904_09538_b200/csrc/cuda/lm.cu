@@ -131,10 +131,25 @@ __global__ void __launch_bounds__(kLmThreads) lm_batched_kernel(LmArgs A) {
 
   if (threadIdx.x < np) {
     const double p0 = A.params[(size_t)b * np + threadIdx.x];
-    scale[threadIdx.x] = A.equilibrate ? (p0 != 0.0 ? fabs(p0) : 1.0) : 1.0;
+    scale[threadIdx.x] = 1.0;
     p[threadIdx.x] = A.opt.nonnegative ? fmax(p0, 0.0) : p0;
   }
   __syncthreads();
+  if (A.equilibrate) {
+    // Column equilibration: iterate on q = p / s with s_i = 1 / ||J[:, i]||
+    // at the start, so every column of the scaled Jacobian has unit norm and
+    // lambda I damps all directions alike (features span ~12 decades).
+    eval_rows(A, f, t, p, scale, w, true);
+    if (threadIdx.x < np) {
+      double s2 = 0.0;
+      for (int k = 0; k < A.nr; ++k) {
+        const double v = w[(size_t)k * stride + threadIdx.x];
+        s2 += v * v;
+      }
+      scale[threadIdx.x] = s2 > 0.0 && isfinite(s2) ? 1.0 / sqrt(s2) : 1.0;
+    }
+    __syncthreads();
+  }
   eval_rows(A, f, t, p, scale, w, false);
   double cost = cost_of(A, w, &red);
   double lambda = A.opt.lambda0;

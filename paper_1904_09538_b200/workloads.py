@@ -45,6 +45,24 @@ def overlap_model(gmem: list[tuple[str, str]], onchip: list[tuple[str, str]]) ->
             f"{co} * sstep({co} - {cg}; p_edge)\n")
 
 
+def smooth_max(a: str, b: str, edge: str) -> str:
+    """a * sstep(a - b; edge) + b * sstep(b - a; edge): max(a, b) as edge -> inf."""
+    return f"({a}) * sstep(({a}) - ({b}); {edge}) + ({b}) * sstep(({b}) - ({a}); {edge})"
+
+
+def overlap3_model(gmem: list[tuple[str, str]], ops: list[tuple[str, str]],
+                   lmem: list[tuple[str, str]]) -> str:
+    """ovh + max(c_gmem, max(c_ops, c_lmem)): the paper's overlap form with the
+    on-chip cost itself split into the FP32 pipe and the shared-memory pipe,
+    which on sm_100 issue concurrently (a kernel bound by LDS wavefronts hides
+    its FFMAs, e.g. the PF matmul)."""
+    ovh = _sum([f"p_bar * {BAR} * {GROUPS}", f"p_group * {GROUPS}", f"p_launch * {LAUNCH}"])
+    cg = _sum([f"{p} * {f}" for p, f in gmem])
+    cops = _sum([f"{p} * {f}" for p, f in ops])
+    cl = _sum([f"{p} * {f}" for p, f in lmem])
+    return OUTPUT + "\n" + ovh + " + " + smooth_max(cg, smooth_max(cops, cl, "p_edge2"), "p_edge") + "\n"
+
+
 ONCHIP = [("p_f32add", OPS["add"]), ("p_f32mul", OPS["mul"]), ("p_f32madd", OPS["madd"]),
           ("p_f32l", LMEM)]
 
@@ -81,7 +99,8 @@ MATMUL = Workload(
     calibration_tags=MICRO_TAGS + [["matmul_sq_rm"]],
     application_tags=[["matmul_sq"]],
     models={"linear": linear_model(MATMUL_GMEM, ONCHIP),
-            "nonlinear": overlap_model(MATMUL_GMEM, ONCHIP)},
+            "nonlinear": overlap_model(MATMUL_GMEM, ONCHIP),
+            "overlap3": overlap3_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:])},
     variant_keys=("prefetch",),
     size_keys=("n",),
 )
