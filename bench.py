@@ -257,8 +257,7 @@ def model_report(wl, cal, app, mean_s: dict[str, float], dev=None) -> dict:
             rep["reference_fit"] = {"error": str(e)}
         if dev is not None:
             from paper_1904_09538_b200.device import fit_lm_batched
-            fs, ts = fc / tc[:, None], np.ones_like(tc)
-            p0 = m.initial_point(fc, tc, scale=True)
+            p0 = m.initial_point(fc, tc, scale=2)  # relative-residual QR start
             starts = [p0]
             edges = [i for i, c in enumerate(m.cost_params) if not c]  # tanh-only params
             if edges:
@@ -268,7 +267,8 @@ def model_report(wl, cal, app, mean_s: dict[str, float], dev=None) -> dict:
                     starts.append(s)
             starts = np.stack(starts)
             t0 = time.perf_counter()
-            params, stats = fit_lm_batched(dev, m, fs, ts, starts, mode=1)
+            # mode 1|4: equilibrated columns, residuals relative to t (weights 1/t)
+            params, stats = fit_lm_batched(dev, m, fc, tc, starts, mode=5)
             dt = time.perf_counter() - t0
             ok = [i for i, s in enumerate(stats) if s["status"] == 0]
             best = min(ok, key=lambda i: stats[i]["residual_norm"]) if ok else 0

@@ -216,33 +216,25 @@ int ps_fit_lm_batched_ex(ps_ctx* ctx, const ps_bytecode* model, const ps_bytecod
                          const ps_fit_opts* opts, int mode, double* params_inout,
                          ps_fit_stats* stats);
 
-/* Batched prediction over a variant space. Each of the nvar variants carries
- * a count table: nf features, each an exact polynomial in the point's
- * parameters with a rational scale (feature = poly(point) / den), see
- * DESIGN.md "K18". points: [npts][nparams] int64; params_fit: [nvar][np];
- * pred: [npts][nvar] seconds; argmin: [npts][ngroups] winning variant index
- * per application group (strict '<' first minimum, tools/perfseer.cpp:458-467). */
-typedef struct ps_variant_tables {
-  int32_t nvar;          /* variants */
-  int32_t nf;            /* features per variant (model feature order) */
-  int32_t nparams;       /* point coordinates */
-  int32_t max_terms;     /* terms per feature polynomial */
-  int32_t ngroups;       /* application groups for argmin */
-  int32_t reserved;
-  const int32_t* var_group;     /* [nvar] group index */
-  const int32_t* var_model;     /* [nvar] model index into models[] */
-  const int32_t* var_coord;     /* [nvar][4] which point coordinate feeds symbol 0..3 (-1 unused) */
-  const int64_t* coef_num;      /* [nvar][nf][max_terms] */
-  const int64_t* coef_den;      /* [nvar][nf] common denominator (already includes granularity) */
-  const int8_t* exps;           /* [nvar][nf][max_terms][4] exponents of symbols 0..3 */
-  int32_t nmodels;
-  int32_t model_np;             /* parameters per model (max) */
-  const ps_bytecode* models;    /* [nmodels] */
-  const double* params;         /* [nmodels][model_np] */
-} ps_variant_tables;
-
-int ps_eval_batched(ps_ctx* ctx, const ps_variant_tables* tables, const int64_t* points,
-                    int64_t npts, double* pred, uint8_t* argmin);
+/* K18 batched prediction over a variant space. A table set is compiled
+ * host-side from JSON {"variants": [{"id": variant id, "model": model text,
+ * "params": [fitted values], "group": application index, "coords":
+ * {"<size parameter>": point coordinate 0..3}}]}: every model feature of
+ * every variant becomes an exact integer polynomial in the point coordinates
+ * (checked against evaluate_feature at several admissible sizes, so a
+ * parameter-dependent match is an error rather than a silent freeze).
+ * points: [npts][4] int64; pred: [npts][nvar] seconds; argmin:
+ * [npts][ngroups] winning variant index per application group (strict '<'
+ * first minimum in variant order, tools/perfseer.cpp:458-467). */
+typedef struct ps_tables ps_tables;
+int ps_tables_build(const char* spec_json, ps_tables** out);
+int ps_tables_info(const ps_tables* tables, int* nvar, int* ngroups, int64_t* nterms);
+int ps_tables_free(ps_tables* tables);
+int ps_eval_batched(ps_ctx* ctx, const ps_tables* tables, const int64_t* points, int64_t npts,
+                    double* pred, uint8_t* argmin, double* kernel_seconds);
+/* The same evaluation on `threads` host threads (CPU port of K18). */
+int ps_eval_cpu(const ps_tables* tables, const int64_t* points, int64_t npts, double* pred,
+                uint8_t* argmin, int threads);
 
 /* --- host pipeline over the C++ port (no GPU) ----------------------------
  * Text in, caller-owned buffers out. Lists are newline-separated. */

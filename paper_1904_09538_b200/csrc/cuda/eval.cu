@@ -1,0 +1,162 @@
+// K18: batched prediction and ranking over a variant space.
+//
+// One thread per parameter point. For every variant the model's count
+// features are evaluated exactly (128-bit integer polynomial / common
+// denominator, the reference's exact-rational evaluation, features.cpp:342-415),
+// converted to double, and the calibrated model is evaluated by a bytecode
+// interpreter (eval_model, model.cpp:409-419). Per application group the
+// winner is the strict '<' first minimum in variant order
+// (tools/perfseer.cpp:458-467). Points are read once (32 B) and predictions
+// written once (8 B per variant): the kernel is integer/FP64 compute bound.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "runtime_internal.h"
+
+namespace ps {
+
+constexpr int kEvalMaxFeat = 48;
+constexpr int kEvalMaxGroups = 8;
+constexpr int kEvalMaxStack = 48;
+
+struct DevTables {
+  FlatTables t;  // pointers are device pointers
+};
+
+__device__ double eval_model_bc(const int32_t* ops, int n_ops, const double* consts, const double* p,
+                                const double* f) {
+  double st[kEvalMaxStack];
+  int sp = 0;
+  for (int i = 0; i < n_ops; ++i) {
+    const int32_t w = ops[i];
+    const int code = w >> 16, arg = w & 0xffff;
+    switch (code) {
+      case PS_BC_NUM: st[sp++] = consts[arg]; break;
+      case PS_BC_PARAM: st[sp++] = p[arg]; break;
+      case PS_BC_FEAT: st[sp++] = f[arg]; break;
+      case PS_BC_TANH: st[sp - 1] = tanh(st[sp - 1]); break;
+      default: {
+        const double b = st[--sp], a = st[sp - 1];
+        st[sp - 1] = code == PS_BC_ADD ? __dadd_rn(a, b)
+                     : code == PS_BC_SUB ? __dsub_rn(a, b)
+                     : code == PS_BC_MUL ? __dmul_rn(a, b)
+                                         : __ddiv_rn(a, b);
+      }
+    }
+  }
+  return st[0];
+}
+
+__global__ void __launch_bounds__(128) eval_points_kernel(FlatTables t, const int64_t* __restrict__ points,
+                                                          int64_t npts, double* __restrict__ pred,
+                                                          uint8_t* __restrict__ argmin) {
+  for (int64_t pt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pt < npts;
+       pt += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[c] = points[pt * 4 + c];
+    double best[kEvalMaxGroups];
+    int besti[kEvalMaxGroups];
+    for (int g = 0; g < t.ngroups; ++g) besti[g] = -1;
+    for (int v = 0; v < t.nvar; ++v) {
+      const int m = t.var_model[v];
+      const int nf = t.model_nf[m];
+      double f[kEvalMaxFeat];
+      for (int j = 0; j < nf; ++j) {
+        const int slot = t.var_feat_base[v] + j;
+        __int128 acc = 0;
+        for (int k = t.feat_begin[slot]; k < t.feat_end[slot]; ++k) {
+          __int128 term = t.term_coef[k];
+          for (int c = 0; c < 4; ++c)
+            for (int e = 0; e < t.term_exp[k * 4 + c]; ++e) term *= x[c];
+          acc += term;
+        }
+        f[j] = (double)(acc / t.feat_den[slot]);
+      }
+      const double y = eval_model_bc(t.ops + t.model_op_begin[m], t.model_op_begin[m + 1] - t.model_op_begin[m],
+                                     t.consts + t.model_const_begin[m], t.params + t.model_param_begin[m], f);
+      pred[pt * t.nvar + v] = y;
+      const int g = t.var_group[v];
+      if (besti[g] < 0 || y < best[g]) {
+        best[g] = y;
+        besti[g] = v;
+      }
+    }
+    for (int g = 0; g < t.ngroups; ++g) argmin[pt * t.ngroups + g] = (uint8_t)besti[g];
+  }
+}
+
+int eval_tables_gpu(Ctx* c, const FlatTables& h, const int64_t* points, int64_t npts, double* pred,
+                    uint8_t* argmin, double* kernel_seconds) {
+  if (h.ngroups > kEvalMaxGroups) return set_error(PS_ERR_ARG, "at most %d application groups", kEvalMaxGroups);
+  for (int m = 0; m < h.nmodels; ++m)
+    if (h.model_nf[m] > kEvalMaxFeat) return set_error(PS_ERR_ARG, "model with more than %d features", kEvalMaxFeat);
+  if (cudaSetDevice(c->device) != cudaSuccess) return set_error(PS_ERR_CUDA, "cudaSetDevice failed");
+  // Pack every table array into one device allocation.
+  struct Part {
+    const void* src;
+    size_t bytes;
+    void** dst;
+  };
+  FlatTables d = h;
+  std::vector<Part> parts = {
+      {h.var_group, sizeof(int32_t) * h.nvar, (void**)&d.var_group},
+      {h.var_model, sizeof(int32_t) * h.nvar, (void**)&d.var_model},
+      {h.var_feat_base, sizeof(int32_t) * h.nvar, (void**)&d.var_feat_base},
+      {h.feat_begin, sizeof(int32_t) * h.nslots, (void**)&d.feat_begin},
+      {h.feat_end, sizeof(int32_t) * h.nslots, (void**)&d.feat_end},
+      {h.feat_den, sizeof(int64_t) * h.nslots, (void**)&d.feat_den},
+      {h.term_coef, sizeof(int64_t) * h.nterms, (void**)&d.term_coef},
+      {h.term_exp, (size_t)4 * h.nterms, (void**)&d.term_exp},
+      {h.model_nf, sizeof(int32_t) * h.nmodels, (void**)&d.model_nf},
+      {h.model_op_begin, sizeof(int32_t) * (h.nmodels + 1), (void**)&d.model_op_begin},
+      {h.ops, sizeof(int32_t) * h.model_op_begin[h.nmodels], (void**)&d.ops},
+      {h.model_const_begin, sizeof(int32_t) * (h.nmodels + 1), (void**)&d.model_const_begin},
+      {h.consts, sizeof(double) * std::max(1, h.model_const_begin[h.nmodels]), (void**)&d.consts},
+      {h.model_param_begin, sizeof(int32_t) * (h.nmodels + 1), (void**)&d.model_param_begin},
+      {h.params, sizeof(double) * h.model_param_begin[h.nmodels], (void**)&d.params},
+  };
+  size_t total = 0;
+  for (auto& p : parts) total += (p.bytes + 255) & ~size_t(255);
+  const size_t pts_bytes = sizeof(int64_t) * 4 * (size_t)npts;
+  const size_t pred_bytes = sizeof(double) * (size_t)npts * h.nvar;
+  const size_t arg_bytes = (size_t)npts * h.ngroups;
+  int rc = c->ensure(c->scratch[1], total + pts_bytes + pred_bytes + arg_bytes + 1024);
+  if (rc) return rc;
+  char* base = static_cast<char*>(c->scratch[1].ptr);
+  size_t off = 0;
+  for (auto& p : parts) {
+    *p.dst = base + off;
+    if (p.bytes && cudaMemcpyAsync(base + off, p.src, p.bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+      return set_error(PS_ERR_CUDA, "table upload failed");
+    off += (p.bytes + 255) & ~size_t(255);
+  }
+  int64_t* dpts = reinterpret_cast<int64_t*>(base + off);
+  off += (pts_bytes + 255) & ~size_t(255);
+  double* dpred = reinterpret_cast<double*>(base + off);
+  off += (pred_bytes + 255) & ~size_t(255);
+  uint8_t* darg = reinterpret_cast<uint8_t*>(base + off);
+  cudaMemcpyAsync(dpts, points, pts_bytes, cudaMemcpyHostToDevice, c->stream);
+  if ((rc = events(c, 2))) return rc;
+  const int threads = 128;
+  const int64_t want = (npts + threads - 1) / threads;
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->sm_count * 16));
+  cudaEventRecord(c->ev[0], c->stream);
+  eval_points_kernel<<<blocks, threads, 0, c->stream>>>(d, dpts, npts, dpred, darg);
+  cudaEventRecord(c->ev[1], c->stream);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "eval launch failed: %s", cudaGetErrorString(e));
+  cudaMemcpyAsync(pred, dpred, pred_bytes, cudaMemcpyDeviceToHost, c->stream);
+  cudaMemcpyAsync(argmin, darg, arg_bytes, cudaMemcpyDeviceToHost, c->stream);
+  e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "eval failed: %s", cudaGetErrorString(e));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+  if (kernel_seconds) *kernel_seconds = ms * 1e-3;
+  return PS_OK;
+}
+
+}  // namespace ps

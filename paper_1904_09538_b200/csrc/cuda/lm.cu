@@ -66,6 +66,7 @@ struct LmArgs {
   ps_fit_opts opt;
   int equilibrate;
   int ordered;             // 1: per-entry sums in row order (reference order)
+  int relative;            // 1: residuals relative to t (weights 1/t)
 };
 
 // Sum over rows k of x(k), either sequentially in row order by one thread
@@ -91,9 +92,13 @@ __device__ void eval_rows(const LmArgs& A, const double* f, const double* t, con
   for (int k = threadIdx.x; k < A.nr; k += blockDim.x) {
     const double* fk = f + (size_t)k * A.nf;
     double* wk = w + (size_t)k * stride;
-    wk[A.np] = t[k] - run_program(A.model, p, fk);
+    // Relative mode: r = (t - g) / t, J = dg/dp / t — the output scaling of
+    // model.cpp:421-435 applied to the model rather than to each feature, so
+    // product terms (p_bar * f_barrier * f_groups) scale correctly.
+    const double w_row = A.relative ? 1.0 / t[k] : 1.0;
+    wk[A.np] = (t[k] - run_program(A.model, p, fk)) * w_row;
     if (jacobian)
-      for (int i = 0; i < A.np; ++i) wk[i] = run_program(A.jac[i], p, fk) * scale[i];
+      for (int i = 0; i < A.np; ++i) wk[i] = run_program(A.jac[i], p, fk) * scale[i] * w_row;
   }
   __syncthreads();
 }
@@ -350,7 +355,7 @@ extern "C" int ps_fit_lm_batched_ex(ps_ctx* ctx, const ps_bytecode* model, const
   cudaMemcpyAsync(dt, t, tbytes, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(dp, params_inout, pbytes, cudaMemcpyHostToDevice, c->stream);
   LmArgs a{host_progs[0], djac, np, nf, nr, nbatch, df, dt, dp, ds, dw, *opts, equilibrate & 1,
-           (equilibrate & 2) ? 0 : 1};
+           (equilibrate & 2) ? 0 : 1, (equilibrate & 4) ? 1 : 0};
   lm_batched_kernel<<<nbatch, kLmThreads, 0, c->stream>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "LM launch failed: %s", cudaGetErrorString(e));

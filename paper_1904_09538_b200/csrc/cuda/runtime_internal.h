@@ -75,3 +75,28 @@ int dg_launch(Ctx* c, const ps_kernel_desc* d);
 int tc_launch(Ctx* c, const ps_kernel_desc* d);
 
 }  // namespace ps
+
+namespace ps {
+
+// Flat view of compiled prediction tables (built host-side by
+// perfseer::build_variant_tables, consumed by the K18 kernel).
+struct FlatTables {
+  int nvar, ngroups, nmodels;
+  const int32_t *var_group, *var_model, *var_feat_base;
+  const int32_t *feat_begin, *feat_end;
+  const int64_t *feat_den, *term_coef;
+  const int8_t* term_exp;  // [nterms][4]
+  int nslots, nterms;
+  const int32_t* model_nf;        // [nmodels]
+  const int32_t* model_op_begin;  // [nmodels + 1] into ops
+  const int32_t* ops;
+  const int32_t* model_const_begin;  // [nmodels + 1] into consts
+  const double* consts;
+  const int32_t* model_param_begin;  // [nmodels + 1] into params
+  const double* params;
+};
+
+int eval_tables_gpu(Ctx* c, const FlatTables& t, const int64_t* points, int64_t npts, double* pred,
+                    uint8_t* argmin, double* kernel_seconds);
+
+}  // namespace ps

@@ -151,7 +151,10 @@ int ps_initial_point(const char* model_text, const double* features, const doubl
     CalibrationProblem p;
     for (int r = 0; r < nr; ++r)
       p.rows.push_back(CalibrationRow{std::vector<double>(features + size_t(r) * nf, features + size_t(r + 1) * nf), t[r]});
-    const auto p0 = initial_point(m, scale ? scale_features_by_output(p) : p);
+    // scale: 0 reference start on raw rows, 1 reference start on output-scaled
+    // rows (what fit_model uses), 2 relative-residual QR start (B200 fit).
+    const auto p0 = scale == 2 ? initial_point_relative(m, p)
+                               : initial_point(m, scale ? scale_features_by_output(p) : p);
     std::copy(p0.begin(), p0.end(), params_out);
     return PS_OK;
   });
@@ -194,6 +197,132 @@ int ps_model_bytecode(const char* model_text, int which, int32_t* ops, int cap_o
 int ps_geo_mean_rel_error(const double* pred, const double* meas, int n, double* out) {
   return guarded([&] {
     *out = geo_mean_rel_error(std::vector<double>(pred, pred + n), std::vector<double>(meas, meas + n));
+    return PS_OK;
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// K18 tables
+
+#include <thread>
+
+#include "ps_tables.hpp"
+
+struct ps_tables {
+  perfseer::VariantTables t;
+  // flattened model programs for the device
+  std::vector<int32_t> model_op_begin, ops, model_const_begin, model_param_begin;
+  std::vector<double> consts, params;
+  std::vector<int8_t> term_exp;
+  ps::FlatTables flat() const {
+    ps::FlatTables f{};
+    f.nvar = int(t.var_model.size());
+    f.ngroups = t.ngroups;
+    f.nmodels = int(t.models.size());
+    f.var_group = t.var_group.data();
+    f.var_model = t.var_model.data();
+    f.var_feat_base = t.var_feat_base.data();
+    f.feat_begin = t.feat_begin.data();
+    f.feat_end = t.feat_end.data();
+    f.feat_den = t.feat_den.data();
+    f.term_coef = t.term_coef.data();
+    f.term_exp = term_exp.data();
+    f.nslots = int(t.feat_begin.size());
+    f.nterms = int(t.term_coef.size());
+    f.model_nf = t.model_nf.data();
+    f.model_op_begin = model_op_begin.data();
+    f.ops = ops.data();
+    f.model_const_begin = model_const_begin.data();
+    f.consts = consts.data();
+    f.model_param_begin = model_param_begin.data();
+    f.params = params.data();
+    return f;
+  }
+};
+
+extern "C" {
+
+int ps_tables_build(const char* spec_json, ps_tables** out) {
+  return guarded([&] {
+    if (!spec_json || !out) throw EvalError("ps_tables_build: null argument");
+    auto* h = new ps_tables();
+    try {
+      h->t = build_variant_tables(spec_json);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    h->model_op_begin.push_back(0);
+    h->model_const_begin.push_back(0);
+    h->model_param_begin.push_back(0);
+    for (size_t m = 0; m < h->t.models.size(); ++m) {
+      const auto& bc = h->t.models[m];
+      h->ops.insert(h->ops.end(), bc.ops.begin(), bc.ops.end());
+      h->consts.insert(h->consts.end(), bc.consts.begin(), bc.consts.end());
+      h->params.insert(h->params.end(), h->t.params[m].begin(), h->t.params[m].end());
+      h->model_op_begin.push_back(int32_t(h->ops.size()));
+      h->model_const_begin.push_back(int32_t(h->consts.size()));
+      h->model_param_begin.push_back(int32_t(h->params.size()));
+    }
+    for (const auto& e : h->t.term_exp) h->term_exp.insert(h->term_exp.end(), e.begin(), e.end());
+    *out = h;
+    return PS_OK;
+  });
+}
+
+int ps_tables_info(const ps_tables* t, int* nvar, int* ngroups, int64_t* nterms) {
+  if (!t) return ps::set_error(PS_ERR_ARG, "null tables");
+  if (nvar) *nvar = int(t->t.var_model.size());
+  if (ngroups) *ngroups = t->t.ngroups;
+  if (nterms) *nterms = int64_t(t->t.term_coef.size());
+  return PS_OK;
+}
+
+int ps_tables_free(ps_tables* t) {
+  delete t;
+  return PS_OK;
+}
+
+int ps_eval_batched(ps_ctx* ctx, const ps_tables* tables, const int64_t* points, int64_t npts,
+                    double* pred, uint8_t* argmin, double* kernel_seconds) {
+  if (!ctx || !tables || !points || !pred || !argmin) return ps::set_error(PS_ERR_ARG, "ps_eval_batched: null argument");
+  return ps::eval_tables_gpu(reinterpret_cast<ps::Ctx*>(ctx), tables->flat(), points, npts, pred, argmin,
+                             kernel_seconds);
+}
+
+// The same evaluation on host threads (exact int128 features, double model).
+int ps_eval_cpu(const ps_tables* tables, const int64_t* points, int64_t npts, double* pred,
+                uint8_t* argmin, int threads) {
+  return guarded([&] {
+    if (!tables || !points || !pred || !argmin) throw EvalError("ps_eval_cpu: null argument");
+    const auto& t = tables->t;
+    const size_t nvar = t.var_model.size();
+    const int ng = t.ngroups;
+    auto work = [&](int64_t lo, int64_t hi) {
+      for (int64_t pt = lo; pt < hi; ++pt) {
+        std::vector<int> besti(size_t(ng), -1);
+        std::vector<double> best(size_t(ng), 0.0);
+        for (size_t v = 0; v < nvar; ++v) {
+          const auto f = eval_point_cpu(t, v, points + pt * 4);
+          const int m = t.var_model[v];
+          const double y = run_bytecode(t.models[size_t(m)], t.params[size_t(m)].data(), f.data());
+          pred[pt * int64_t(nvar) + int64_t(v)] = y;
+          const int g = t.var_group[v];
+          if (besti[size_t(g)] < 0 || y < best[size_t(g)]) {
+            best[size_t(g)] = y;
+            besti[size_t(g)] = int(v);
+          }
+        }
+        for (int g = 0; g < ng; ++g) argmin[pt * ng + g] = uint8_t(besti[size_t(g)]);
+      }
+    };
+    const int n = std::max(1, threads);
+    std::vector<std::thread> pool;
+    for (int i = 0; i < n; ++i)
+      pool.emplace_back(work, npts * i / n, npts * (i + 1) / n);
+    for (auto& th : pool) th.join();
     return PS_OK;
   });
 }

@@ -97,7 +97,9 @@ class HostModel:
         return p, {"residual_norm": st.residual_norm, "iterations": st.iterations,
                    "converged": bool(st.converged)}
 
-    def initial_point(self, features: np.ndarray, t: np.ndarray, scale: bool = True) -> np.ndarray:
+    def initial_point(self, features: np.ndarray, t: np.ndarray, scale: int = 1) -> np.ndarray:
+        """scale 0/1: the reference's start (model.cpp:439-481) on raw/output-scaled
+        rows; 2: relative-residual QR start used by the B200 fit."""
         f = np.ascontiguousarray(features, dtype=np.float64)
         tt = np.ascontiguousarray(t, dtype=np.float64)
         p = np.zeros(len(self.params), dtype=np.float64)

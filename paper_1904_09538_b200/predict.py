@@ -1,0 +1,96 @@
+"""Batched prediction and ranking over a variant space (K18) through the C ABI.
+
+A table set binds calibrated models to kernel variants (ps_tables_build);
+``eval_gpu`` evaluates every variant at every parameter point on a B200 and
+returns predictions plus the per-application winner; ``eval_cpu`` is the same
+computation on host threads.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+
+import numpy as np
+
+from ._abi import check, lib
+
+_P = C.POINTER
+
+
+def _declare():
+    L = lib()
+    if getattr(L, "_k18_declared", False):
+        return L
+    L.ps_tables_build.argtypes = [C.c_char_p, _P(C.c_void_p)]
+    L.ps_tables_info.argtypes = [C.c_void_p, _P(C.c_int), _P(C.c_int), _P(C.c_int64)]
+    L.ps_tables_free.argtypes = [C.c_void_p]
+    L.ps_eval_batched.argtypes = [C.c_void_p, C.c_void_p, _P(C.c_int64), C.c_int64,
+                                  _P(C.c_double), _P(C.c_uint8), _P(C.c_double)]
+    L.ps_eval_cpu.argtypes = [C.c_void_p, _P(C.c_int64), C.c_int64, _P(C.c_double),
+                              _P(C.c_uint8), C.c_int]
+    for n in ("ps_tables_build", "ps_tables_info", "ps_tables_free", "ps_eval_batched",
+              "ps_eval_cpu"):
+        getattr(L, n).restype = C.c_int
+    L._k18_declared = True
+    return L
+
+
+class PredictionTables:
+    """variants: list of dicts {id, model (text), params (list), group, coords}."""
+
+    def __init__(self, variants: list[dict]):
+        L = _declare()
+        self._h = C.c_void_p()
+        check(L.ps_tables_build(json.dumps({"variants": variants}).encode(), C.byref(self._h)))
+        nvar, ngroups, nterms = C.c_int(), C.c_int(), C.c_int64()
+        check(L.ps_tables_info(self._h, C.byref(nvar), C.byref(ngroups), C.byref(nterms)))
+        self.nvar, self.ngroups, self.nterms = nvar.value, ngroups.value, nterms.value
+        self.ids = [v["id"] for v in variants]
+
+    def close(self):
+        if self._h:
+            _declare().ps_tables_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _out(self, points: np.ndarray):
+        pts = np.ascontiguousarray(points, dtype=np.int64)
+        if pts.ndim != 2 or pts.shape[1] != 4:
+            raise ValueError("points must be [npts, 4] int64")
+        pred = np.empty((pts.shape[0], self.nvar), dtype=np.float64)
+        arg = np.empty((pts.shape[0], self.ngroups), dtype=np.uint8)
+        return pts, pred, arg
+
+    def eval_gpu(self, dev, points: np.ndarray):
+        pts, pred, arg = self._out(points)
+        secs = C.c_double()
+        check(_declare().ps_eval_batched(dev._ctx, self._h, pts.ctypes.data_as(_P(C.c_int64)),
+                                         pts.shape[0], pred.ctypes.data_as(_P(C.c_double)),
+                                         arg.ctypes.data_as(_P(C.c_uint8)), C.byref(secs)))
+        return pred, arg, secs.value
+
+    def eval_cpu(self, points: np.ndarray, threads: int = 1):
+        pts, pred, arg = self._out(points)
+        check(_declare().ps_eval_cpu(self._h, pts.ctypes.data_as(_P(C.c_int64)), pts.shape[0],
+                                     pred.ctypes.data_as(_P(C.c_double)),
+                                     arg.ctypes.data_as(_P(C.c_uint8)), threads))
+        return pred, arg
+
+
+def c5_points(npts: int, seed: int = 7) -> np.ndarray:
+    """BASELINE.json configs[4] parameter points: n_mm in 16Z
+    within [512, 8192], n_fd in 112Z within [1120, 8176], nel in 16Z within
+    [1e4, 1e6], DG order 1..7 as padded nodes per element."""
+    rng = np.random.default_rng(seed)
+    np_of_order = np.array([16, 16, 32, 48, 64, 96, 128])  # (k+1)(k+2)(k+3)/6 padded to 16
+    p = np.empty((npts, 4), dtype=np.int64)
+    p[:, 0] = 16 * rng.integers(512 // 16, 8192 // 16 + 1, npts)
+    p[:, 1] = 112 * rng.integers(1120 // 112, 8176 // 112 + 1, npts)
+    p[:, 2] = 16 * rng.integers(10000 // 16 + 1, 1000000 // 16 + 1, npts)
+    p[:, 3] = np_of_order[rng.integers(0, 7, npts)]
+    return p

@@ -46,8 +46,13 @@ def overlap_model(gmem: list[tuple[str, str]], onchip: list[tuple[str, str]]) ->
 
 
 def smooth_max(a: str, b: str, edge: str) -> str:
-    """a * sstep(a - b; edge) + b * sstep(b - a; edge): max(a, b) as edge -> inf."""
-    return f"({a}) * sstep(({a}) - ({b}); {edge}) + ({b}) * sstep(({b}) - ({a}); {edge})"
+    """max(a, b) through the paper's tanh step (Eq. 5) on the NORMALISED
+    difference (a - b) / (a + b): the step argument is dimensionless, so one
+    p_edge is equally sharp for a 5 us and a 200 ms kernel (the paper's
+    sstep(a - b) needs p_edge ~ 1/t)."""
+    s = f"(({a}) + ({b}))"
+    return (f"({a}) * sstep((({a}) - ({b})) / {s}; {edge}) + "
+            f"({b}) * sstep((({b}) - ({a})) / {s}; {edge})")
 
 
 def overlap3_model(gmem: list[tuple[str, str]], ops: list[tuple[str, str]],
