@@ -267,8 +267,9 @@ def model_report(wl, cal, app, mean_s: dict[str, float], dev=None) -> dict:
                     starts.append(s)
             starts = np.stack(starts)
             t0 = time.perf_counter()
-            # mode 1|4: equilibrated columns, residuals relative to t (weights 1/t)
-            params, stats = fit_lm_batched(dev, m, fc, tc, starts, mode=5)
+            # mode 1|4|8: equilibrated columns, residuals relative to t
+            # (weights 1/t), forward-mode derivatives on the device
+            params, stats = fit_lm_batched(dev, m, fc, tc, starts, mode=13)
             dt = time.perf_counter() - t0
             ok = [i for i, s in enumerate(stats) if s["status"] == 0]
             best = min(ok, key=lambda i: stats[i]["residual_norm"]) if ok else 0

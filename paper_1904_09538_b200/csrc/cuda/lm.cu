@@ -54,6 +54,60 @@ __device__ double run_program(const LmProgram& pr, const double* p, const double
   return st[0];
 }
 
+// Forward-mode differentiation of the model bytecode: every stack slot
+// carries its value and its gradient with respect to the np parameters, so
+// one pass yields g and dg/dp without the symbolic derivative trees (which
+// grow combinatorially for nested overlap steps). The product, quotient and
+// tanh rules are the ones diff_expr applies (model.cpp:289-330).
+constexpr int kDualStack = 24;
+__device__ void run_dual(const LmProgram& pr, const double* p, const double* f, int np, double* val,
+                         double* grad) {
+  double sv[kDualStack];
+  double sg[kDualStack][kLmMaxParams];
+  int sp = 0;
+  for (int i = 0; i < pr.n_ops; ++i) {
+    const int32_t w = pr.ops[i];
+    const int code = w >> 16, arg = w & 0xffff;
+    switch (code) {
+      case PS_BC_NUM:
+      case PS_BC_FEAT:
+        sv[sp] = code == PS_BC_NUM ? pr.consts[arg] : f[arg];
+        for (int j = 0; j < np; ++j) sg[sp][j] = 0.0;
+        ++sp;
+        break;
+      case PS_BC_PARAM:
+        sv[sp] = p[arg];
+        for (int j = 0; j < np; ++j) sg[sp][j] = j == arg ? 1.0 : 0.0;
+        ++sp;
+        break;
+      case PS_BC_TANH: {
+        const double t = tanh(sv[sp - 1]);
+        const double d = 1.0 - t * t;
+        sv[sp - 1] = t;
+        for (int j = 0; j < np; ++j) sg[sp - 1][j] = d * sg[sp - 1][j];
+        break;
+      }
+      default: {
+        const int bi = --sp, ai = sp - 1;
+        const double a = sv[ai], b = sv[bi];
+        if (code == PS_BC_ADD || code == PS_BC_SUB) {
+          const double s = code == PS_BC_ADD ? 1.0 : -1.0;
+          for (int j = 0; j < np; ++j) sg[ai][j] = sg[ai][j] + s * sg[bi][j];
+          sv[ai] = code == PS_BC_ADD ? a + b : a - b;
+        } else if (code == PS_BC_MUL) {
+          for (int j = 0; j < np; ++j) sg[ai][j] = sg[ai][j] * b + a * sg[bi][j];
+          sv[ai] = a * b;
+        } else {
+          for (int j = 0; j < np; ++j) sg[ai][j] = sg[ai][j] / b - a * sg[bi][j] / (b * b);
+          sv[ai] = a / b;
+        }
+      }
+    }
+  }
+  *val = sv[0];
+  for (int j = 0; j < np; ++j) grad[j] = sg[0][j];
+}
+
 struct LmArgs {
   LmProgram model;
   const LmProgram* jac;  // [np]
@@ -67,6 +121,7 @@ struct LmArgs {
   int equilibrate;
   int ordered;             // 1: per-entry sums in row order (reference order)
   int relative;            // 1: residuals relative to t (weights 1/t)
+  int dual;                // 1: forward-mode derivatives (jac programs unused)
 };
 
 // Sum over rows k of x(k), either sequentially in row order by one thread
@@ -96,6 +151,13 @@ __device__ void eval_rows(const LmArgs& A, const double* f, const double* t, con
     // model.cpp:421-435 applied to the model rather than to each feature, so
     // product terms (p_bar * f_barrier * f_groups) scale correctly.
     const double w_row = A.relative ? 1.0 / t[k] : 1.0;
+    if (jacobian && A.dual) {
+      double g, grad[kLmMaxParams];
+      run_dual(A.model, p, fk, A.np, &g, grad);
+      wk[A.np] = (t[k] - g) * w_row;
+      for (int i = 0; i < A.np; ++i) wk[i] = grad[i] * scale[i] * w_row;
+      continue;
+    }
     wk[A.np] = (t[k] - run_program(A.model, p, fk)) * w_row;
     if (jacobian)
       for (int i = 0; i < A.np; ++i) wk[i] = run_program(A.jac[i], p, fk) * scale[i] * w_row;
@@ -299,7 +361,8 @@ extern "C" int ps_fit_lm_batched_ex(ps_ctx* ctx, const ps_bytecode* model, const
                                     int nbatch, const ps_fit_opts* opts, int equilibrate,
                                     double* params_inout, ps_fit_stats* stats) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
-  if (!c || !model || !jac || !features || !t || !opts || !params_inout || !stats)
+  const bool dual = (equilibrate & 8) != 0;
+  if (!c || !model || (!jac && !dual) || !features || !t || !opts || !params_inout || !stats)
     return set_error(PS_ERR_ARG, "ps_fit_lm_batched: null argument");
   if (np < 1 || np > kLmMaxParams) return set_error(PS_ERR_ARG, "np must be in 1..%d", kLmMaxParams);
   if (nr < np)
@@ -311,7 +374,8 @@ extern "C" int ps_fit_lm_batched_ex(ps_ctx* ctx, const ps_bytecode* model, const
   cudaSetDevice(c->device);
   // Device copies: programs, features, t, params, stats.
   std::vector<const ps_bytecode*> progs{model};
-  for (int i = 0; i < np; ++i) progs.push_back(&jac[i]);
+  if (!dual)
+    for (int i = 0; i < np; ++i) progs.push_back(&jac[i]);
   size_t op_words = 0, const_words = 0;
   for (auto* p : progs) {
     op_words += (size_t)p->n_ops;
@@ -350,12 +414,13 @@ extern "C" int ps_fit_lm_batched_ex(ps_ctx* ctx, const ps_bytecode* model, const
   double* dp = reinterpret_cast<double*>(carve(pbytes));
   ps_fit_stats* ds = reinterpret_cast<ps_fit_stats*>(carve(sbytes));
   double* dw = reinterpret_cast<double*>(carve(wbytes));
-  cudaMemcpyAsync(djac, host_progs.data() + 1, sizeof(LmProgram) * np, cudaMemcpyHostToDevice, c->stream);
+  if (!dual)
+    cudaMemcpyAsync(djac, host_progs.data() + 1, sizeof(LmProgram) * np, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(df, features, fbytes, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(dt, t, tbytes, cudaMemcpyHostToDevice, c->stream);
   cudaMemcpyAsync(dp, params_inout, pbytes, cudaMemcpyHostToDevice, c->stream);
   LmArgs a{host_progs[0], djac, np, nf, nr, nbatch, df, dt, dp, ds, dw, *opts, equilibrate & 1,
-           (equilibrate & 2) ? 0 : 1, (equilibrate & 4) ? 1 : 0};
+           (equilibrate & 2) ? 0 : 1, (equilibrate & 4) ? 1 : 0, (equilibrate & 8) ? 1 : 0};
   lm_batched_kernel<<<nbatch, kLmThreads, 0, c->stream>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "LM launch failed: %s", cudaGetErrorString(e));

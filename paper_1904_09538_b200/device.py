@@ -180,7 +180,12 @@ def fit_lm_batched(dev: CudaDevice, model, features: np.ndarray, t: np.ndarray, 
                         consts.ctypes.data_as(C.POINTER(C.c_double)))
 
     mb = bc(-1)
-    jac = (Bytecode * npar)(*[bc(i) for i in range(npar)])
+    if mode & 8:  # forward-mode derivatives on the device: no derivative programs
+        if model.bytecode(-1)[2] > 24:
+            raise ValueError("model expression too deep for the device evaluator (stack > 24)")
+        jac = None
+    else:
+        jac = (Bytecode * npar)(*[bc(i) for i in range(npar)])
     params = np.ascontiguousarray(p0.copy())
     stats = (FitStats * nb)()
     o = opts or default_fit_opts()

@@ -117,13 +117,18 @@ class HostModel:
 
     def bytecode(self, which: int = -1):
         cap = 1 << 14
-        ops = np.zeros(cap, dtype=np.int32)
-        consts = np.zeros(cap, dtype=np.float64)
-        n_ops, n_consts, stack = C.c_int(), C.c_int(), C.c_int()
-        check(_declare().ps_model_bytecode(self.text.encode(), which,
-                                           ops.ctypes.data_as(_P(C.c_int32)), cap, _dptr(consts),
-                                           cap, C.byref(n_ops), C.byref(n_consts), C.byref(stack)))
-        return ops[: n_ops.value].copy(), consts[: n_consts.value].copy(), stack.value
+        while True:
+            ops = np.zeros(cap, dtype=np.int32)
+            consts = np.zeros(cap, dtype=np.float64)
+            n_ops, n_consts, stack = C.c_int(), C.c_int(), C.c_int()
+            rc = _declare().ps_model_bytecode(self.text.encode(), which,
+                                              ops.ctypes.data_as(_P(C.c_int32)), cap, _dptr(consts),
+                                              cap, C.byref(n_ops), C.byref(n_consts), C.byref(stack))
+            if rc and max(n_ops.value, n_consts.value) > cap:
+                cap = max(n_ops.value, n_consts.value)
+                continue
+            check(rc)
+            return ops[: n_ops.value].copy(), consts[: n_consts.value].copy(), stack.value
 
 
 def default_fit_opts() -> FitOpts:

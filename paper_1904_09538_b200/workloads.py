@@ -50,9 +50,35 @@ def smooth_max(a: str, b: str, edge: str) -> str:
     difference (a - b) / (a + b): the step argument is dimensionless, so one
     p_edge is equally sharp for a 5 us and a 200 ms kernel (the paper's
     sstep(a - b) needs p_edge ~ 1/t)."""
-    s = f"(({a}) + ({b}))"
+    s = f"(({a}) + ({b}) + 1e-15)"  # + 1 fs: defined when both costs vanish
     return (f"({a}) * sstep((({a}) - ({b})) / {s}; {edge}) + "
             f"({b}) * sstep((({b}) - ({a})) / {s}; {edge})")
+
+
+def sharp_max(a: str, b: str, k: float = 40.0) -> str:
+    """smooth_max with a fixed sharpness k on the normalised difference: a 5%
+    cost gap already selects the larger term to 99%, i.e. the sm_100 pipes
+    (LSU/L1, shared, FMA) are taken to overlap completely; no edge parameter
+    is fitted."""
+    s = f"(({a}) + ({b}) + 1e-15)"
+    return (f"({a}) * (tanh({k} * (({a}) - ({b})) / {s}) + 1) / 2 + "
+            f"({b}) * (tanh({k} * (({b}) - ({a})) / {s}) + 1) / 2")
+
+
+def max3_model(gmem: list[tuple[str, str]], ops: list[tuple[str, str]],
+               lmem: list[tuple[str, str]], k: float = 40.0) -> str:
+    """launch/group overhead + max(c_gmem, c_ops, c_lmem, c_barrier) with
+    fixed-sharpness steps: on sm_100 the LSU/L1 path, the FMA pipe and the
+    shared-memory pipe run concurrently, and a work-group waiting at a
+    barrier costs nothing extra while other resident groups keep the binding
+    pipe busy."""
+    ovh = _sum([f"p_group * {GROUPS}", f"p_launch * {LAUNCH}"])
+    cg = _sum([f"{p} * {f}" for p, f in gmem])
+    cops = _sum([f"{p} * {f}" for p, f in ops])
+    cl = _sum([f"{p} * {f}" for p, f in lmem])
+    cb = f"p_bar * {BAR} * {GROUPS}"
+    onchip = sharp_max(cops, sharp_max(cl, cb, k), k)
+    return OUTPUT + "\n" + ovh + " + " + sharp_max(cg, onchip, k) + "\n"
 
 
 def overlap3_model(gmem: list[tuple[str, str]], ops: list[tuple[str, str]],
@@ -105,7 +131,8 @@ MATMUL = Workload(
     application_tags=[["matmul_sq"]],
     models={"linear": linear_model(MATMUL_GMEM, ONCHIP),
             "nonlinear": overlap_model(MATMUL_GMEM, ONCHIP),
-            "overlap3": overlap3_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:])},
+            "overlap3": overlap3_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:]),
+            "max3": max3_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:])},
     variant_keys=("prefetch",),
     size_keys=("n",),
 )

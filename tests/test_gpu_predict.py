@@ -1,0 +1,65 @@
+"""K18 batched prediction: GPU tables vs the CPU port of the same tables vs
+the reference-API predict() (features via evaluate_feature), and ranking."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_1904_09538_b200.device import CudaDevice
+    d = CudaDevice(0)
+    yield d
+    d.close()
+
+
+def _tables():
+    from paper_1904_09538_b200 import host, workloads as W
+    from paper_1904_09538_b200.predict import PredictionTables
+    variants = []
+    for name in ("linear", "overlap3"):
+        text = W.MATMUL.models[name]
+        m = host.HostModel(text)
+        rng = np.random.default_rng(3)
+        params = list(rng.uniform(1e-13, 1e-11, len(m.params)))
+        for i, c in enumerate(m.cost_params):
+            if not c:
+                params[i] = 20.0
+        for vid, _ in host.catalog(["matmul_sq", "n:1024"]):
+            variants.append({"id": vid, "model": text, "params": params,
+                             "group": 0 if name == "linear" else 1, "coords": {"n": 0}})
+    return PredictionTables(variants), variants
+
+
+def test_gpu_eval_matches_cpu_tables_and_reference_predict(dev):
+    from paper_1904_09538_b200 import host
+    from paper_1904_09538_b200.predict import c5_points
+    t, variants = _tables()
+    pts = c5_points(20000, seed=11)
+    pg, ag, secs = t.eval_gpu(dev, pts)
+    pc, ac = t.eval_cpu(pts, threads=4)
+    np.testing.assert_allclose(pg, pc, rtol=1e-12, atol=0)
+    # ranking: exact unless the two predictions are within 1e-12
+    near = np.abs(pc[:, 0] - pc[:, 1]) <= 1e-12 * np.abs(pc[:, 0])
+    assert np.array_equal(ag[~near], ac[~near])
+    assert secs > 0
+    # reference-API predict() at a few points
+    for j in range(5):
+        n = int(pts[j, 0])
+        for v, var in enumerate(variants):
+            m = host.HostModel(var["model"])
+            ref = m.predict_cpu(np.array(var["params"]), [var["id"].replace("n-1024", f"n-{n}")])[0]
+            assert abs(pg[j, v] - ref) <= 1e-12 * abs(ref)
+
+
+def test_nontabulable_features_are_rejected():
+    from paper_1904_09538_b200 import PsError
+    from paper_1904_09538_b200.predict import PredictionTables
+    # lstride constraint against a parameter: match flips with n -> error
+    text = ("f_exec_wall_time_cuda_b200_0\n"
+            "p_a * f_mem_access_global_float32_load_lstrides:{1:<1000} + p_b * f_sync_kernel_launch\n")
+    vid = "matmul_sq__dtype-float32__groups_fit-True__lsize_0-16__lsize_1-16__n-512__prefetch-True"
+    with pytest.raises(PsError, match="not tabulable"):
+        PredictionTables([{"id": vid, "model": text, "params": [1.0, 1.0], "group": 0,
+                           "coords": {"n": 0}}])
