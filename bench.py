@@ -474,22 +474,42 @@ def run_ours(args, dist: Dist) -> None:
             fl += ios[k].flops * len(ts)
             fl_t += sum(ts)
 
-    # dominant HBM kernel: the largest gmem_pattern launch
+    # roofline of the dominant kernel (largest share of the timed device time)
     pk, src = peaks()
-    gm = [k for k in trials if descs[k].gen == 1]
-    dom = max(gm, key=lambda k: ios[k].bytes_global) if gm else None
-    roofline = None
-    if dom is not None:
-        avg = sum(trials[dom]) / len(trials[dom])
-        achieved = ios[dom].bytes_global / avg / 1e9
-        traffic = None
-        tf = ROOT / "profiles" / "ncu_traffic.json"
-        if tf.exists():
-            traffic = json.loads(tf.read_text()).get(kernels[dom])
-        roofline = {"kernel": kernels[dom], "bound": "hbm", "achieved": round(achieved, 1),
+    share = {k: sum(ts) for k, ts in trials.items()}
+    total_t = sum(share.values())
+    sm_mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
+    fp32_peak_tf = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # CUDA-core FFMA, measured clock
+
+    def roofline_of(k: int) -> dict:
+        avg = sum(trials[k]) / len(trials[k])
+        d = descs[k]
+        if d.gen in (1, 6, 9, 10):  # streaming kernels: HBM roofline
+            achieved = ios[k].bytes_global / avg / 1e9
+            traffic = None
+            tf = ROOT / "profiles" / "ncu_traffic.json"
+            if tf.exists():
+                traffic = json.loads(tf.read_text()).get(kernels[k])
+            return {"kernel": kernels[k], "bound": "hbm", "achieved": round(achieved, 1),
                     "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
                     "traffic": traffic, "peak_source": src,
-                    "bytes_per_launch": ios[dom].bytes_global}
+                    "algorithmic_bytes_per_launch": ios[k].bytes_global,
+                    "share_of_step": round(share[k] / total_t, 4)}
+        achieved = ios[k].flops / avg / 1e12
+        return {"kernel": kernels[k], "bound": "fp32", "achieved": round(achieved, 3),
+                "peak": round(fp32_peak_tf, 2), "unit": "TFLOP/s",
+                "frac": round(achieved / fp32_peak_tf, 4), "traffic": None,
+                "peak_source": "148 SMs x 128 FP32 lanes x 2 x median SM clock of the run "
+                               "(SURVEY 8(d) C2; no tensor cores in the paper variants)",
+                "algorithmic_flops_per_launch": ios[k].flops,
+                "share_of_step": round(share[k] / total_t, 4),
+                "note": "16x16 CUDA-core tiles by construction (uipick.cpp:464-554); the paper "
+                        "reports 8-20% of FP32 peak for these variants (PAPER.md:2155-2157)"}
+
+    dom = max(share, key=share.get)
+    roofline = roofline_of(dom)
+    gm = [k for k in trials if descs[k].gen == 1]
+    roofline_hbm = roofline_of(max(gm, key=lambda k: ios[k].bytes_global)) if gm else None
 
     if args.table:
         # measurements_to_csv format (executor.cpp:279-295) + raw trials
@@ -513,7 +533,13 @@ def run_ours(args, dist: Dist) -> None:
         "suite_hbm_GBps": round(hbm_b / hbm_t / 1e9, 1) if hbm_t else None,
         "suite_flops_TFps": round(fl / fl_t / 1e12, 2) if fl_t else None,
         "models": models,
+        "geomean_rel_error": (models.get(args.headline_model, {}).get("gpu_multistart_fit", {})
+                              .get("geomean_rel_error")),
+        "ranking_correct": (models.get(args.headline_model, {}).get("gpu_multistart_fit", {})
+                            .get("ranking_correct")),
+        "headline_model": args.headline_model,
         "roofline": roofline,
+        "roofline_hbm": roofline_hbm,
         "cpu_baseline": cpu_gmem_sample() if dist.world == 1 else None,
         "e2e": {"value": round(e2e_bytes_all / e2e_time_max / 1e9, 3) if e2e_time_max else None,
                 "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
@@ -535,6 +561,7 @@ def main() -> None:
     ap.add_argument("--workload", default="matmul")
     ap.add_argument("--trials-per-step", type=int, default=4)
     ap.add_argument("--table", default="", help="write the measurement table (CSV) here")
+    ap.add_argument("--headline-model", default="max3")
     args = ap.parse_args()
     dist = Dist()
     try:
