@@ -27,3 +27,12 @@ $(OUT)/port_gen_golden: $(ROOT)/oracle/gen_golden.cpp $(LIB)
 	$(CXX) $(CXXFLAGS) $< -L$(dir $(LIB)) -lperfseer_b200 -Wl,-rpath,$(dir $(LIB)) -o $@
 
 all: $(OUT)/port_gen_golden
+
+# This repo's own generators (DG included) against the port's enumeration
+# oracle; needs only the port and the doctest shim (no reference sources).
+$(OUT)/port_extra: $(ROOT)/tests/port_extra.cpp $(LIB)
+	@mkdir -p $(OUT)
+	$(CXX) -std=c++20 -O1 -w -I$(ROOT)/paper_1904_09538_b200/csrc/host -I$(ROOT)/oracle/shim -I$(JSON_DIR) $< -L$(dir $(LIB)) -lperfseer_b200 -Wl,-rpath,$(dir $(LIB)) -o $@
+
+extra: $(OUT)/port_extra
+.PHONY: extra
