@@ -173,6 +173,8 @@ class ClockSampler:
 def workload_kernels(name: str):
     from paper_1904_09538_b200 import host, workloads
     wl = workloads.WORKLOADS[name]
+    for key, value in wl.extra.get("options", {}).items():
+        host.set_option(key, value)
     cal = [k for tags in wl.calibration_tags for k, _ in host.catalog(tags)]
     app = [k for tags in wl.application_tags for k, _ in host.catalog(tags)]
     return wl, cal, app

@@ -265,6 +265,10 @@ int ps_predict_cpu(const char* model_text, const double* params, const char* var
 /* Postfix bytecode of the model (which = -1) or of d model / d p_which. */
 int ps_model_bytecode(const char* model_text, int which, int32_t* ops, int cap_ops, double* consts,
                       int cap_consts, int* n_ops, int* n_consts, int* max_stack);
+/* Process-wide options of the host port. "partial_subgroups" = "strict"
+ * (reference: sub-group counts need wg % 32 == 0, features.cpp:318-326) or
+ * "round_up" (a work-group issues ceil(wg/32) sub-groups). */
+int ps_set_option(const char* key, const char* value);
 /* geo_mean_rel_error (executor.cpp:50-61). */
 int ps_geo_mean_rel_error(const double* pred, const double* meas, int n, double* out);
 

@@ -340,6 +340,67 @@ __global__ void __launch_bounds__(T* T) finite_diff(const float* __restrict__ u,
   }
 }
 
+// K12, coarsened: a CTA of T x T threads executes R horizontally adjacent
+// work-groups (j_out = R*bx + r). Every work-item still fetches its own u
+// element into its group's tile and the interior work-items compute their
+// stencil point with the identical operation sequence; the R groups'
+// barriers are executed as one CTA barrier (a superset synchronisation). The
+// R independent fetches per thread keep enough HBM reads in flight.
+template <int T, int R>
+__global__ void __launch_bounds__(T* T) finite_diff_multi(const float* __restrict__ u,
+                                                         float* __restrict__ res, int n) {
+  constexpr int I = T - 2;
+  __shared__ float uf[R][T][T + 1];
+  const int l0 = threadIdx.x, l1 = threadIdx.y;
+  const int i_out = blockIdx.y;
+  const int groups = n / I;
+  const int64_t W = n + 2;
+  const float* urow = u + (int64_t)(I * i_out + l1) * W + l0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int j_out = blockIdx.x * R + r;
+    if (j_out < groups) uf[r][l1][l0] = __ldg(urow + I * j_out);
+  }
+  bar_sync();
+  if (l1 < I && l0 < I) {
+    float* rrow = res + (int64_t)(I * i_out + l1) * n + l0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int j_out = blockIdx.x * R + r;
+      if (j_out >= groups) break;
+      float s = __fadd_rn(uf[r][l1][l0 + 1], uf[r][l1 + 1][l0]);
+      s = __fmaf_rn(-4.0f, uf[r][l1 + 1][l0 + 1], s);
+      s = __fadd_rn(s, uf[r][l1 + 1][l0 + 2]);
+      s = __fadd_rn(s, uf[r][l1 + 2][l0 + 1]);
+      __stcs(rrow + I * j_out, s);
+    }
+  }
+}
+
+template <int T, int R>
+__global__ void __launch_bounds__(T* T) finite_diff_rm_u_multi(const float* __restrict__ u,
+                                                              float* __restrict__ dest, int n) {
+  constexpr int I = T - 2;
+  const int l0 = threadIdx.x, l1 = threadIdx.y;
+  const int i_out = blockIdx.y;
+  const int groups = n / I;
+  const int64_t W = n + 2;
+  const int64_t DW = (int64_t)groups * T;
+  const float* urow = u + (int64_t)(I * i_out + l1) * W + l0;
+  float v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int j_out = blockIdx.x * R + r;
+    v[r] = j_out < groups ? __ldg(urow + I * j_out) : 0.f;
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int j_out = blockIdx.x * R + r;
+    if (j_out < groups)
+      __stcs(dest + (int64_t)(T * i_out + l1) * DW + T * j_out + l0, __fadd_rn(0.0f, v[r]));
+  }
+}
+
 // K13 finite_diff_rm (uipick.cpp:641-664). keep u: tgt_read = 0 + u[fetch
 // index]; tgt_read_dest[T i_out + l1, T j_out + l0] = tgt_read. keep res:
 // res[interior] = tgt_read = 0.

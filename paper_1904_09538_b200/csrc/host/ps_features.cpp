@@ -2,6 +2,7 @@
 // features.cpp:41-493; grammar SPEC.md:323-331).
 #include "ps_features.hpp"
 
+#include <atomic>
 #include <sstream>
 
 #include "ps_executor.hpp"
@@ -244,14 +245,25 @@ namespace {
 
 // Sub-group entries count once per 32 (configurable) work-items; the
 // division must be exact and the work-group a whole number of sub-groups.
+std::atomic<bool> g_round_up_subgroups{false};
+
 Rational per_granularity(const Rational& raw, Granularity g, const KernelCounts& c, int sgs,
                          const std::string& what) {
   long long div = 1;
   if (g == Granularity::sub_group) {
     div = sgs;
-    if (c.geometry && c.geometry->flat_work_group_size() % sgs != 0)
-      throw EvalError("work-group size " + std::to_string(c.geometry->flat_work_group_size()) +
-                      " is not a multiple of the sub-group size " + std::to_string(sgs));
+    const long long wg = c.geometry ? c.geometry->flat_work_group_size() : 0;
+    if (wg && wg % sgs != 0) {
+      // Reference semantics: an error (features.cpp:318-326).
+      // Opt-in extension: a work-group of wg work-items issues
+      // ceil(wg / sgs) sub-groups; counts that are per-work-item multiples of
+      // wg are converted at that rate, others must divide by sgs exactly.
+      if (!g_round_up_subgroups.load())
+        throw EvalError("work-group size " + std::to_string(wg) +
+                        " is not a multiple of the sub-group size " + std::to_string(sgs));
+      Rational per_group = raw / Rational(wg);
+      if (is_integer(per_group)) return per_group * Rational((wg + sgs - 1) / sgs);
+    }
   } else if (g == Granularity::work_group) {
     if (!c.geometry) throw EvalError("work-group granularity needs launch geometry");
     div = c.geometry->flat_work_group_size();
@@ -395,4 +407,9 @@ FeatureTable gather_feature_values(const std::vector<FeatureSpec>& features,
   return t;
 }
 
+}  // namespace perfseer
+
+namespace perfseer {
+void set_partial_subgroup_round_up(bool on) { g_round_up_subgroups.store(on); }
+bool partial_subgroup_round_up() { return g_round_up_subgroups.load(); }
 }  // namespace perfseer

@@ -194,6 +194,19 @@ int ps_model_bytecode(const char* model_text, int which, int32_t* ops, int cap_o
   });
 }
 
+int ps_set_option(const char* key, const char* value) {
+  return guarded([&] {
+    const std::string k = key ? key : "", v = value ? value : "";
+    if (k == "partial_subgroups") {
+      if (v != "strict" && v != "round_up") throw EvalError("partial_subgroups: strict | round_up");
+      set_partial_subgroup_round_up(v == "round_up");
+      clear_count_cache();
+      return PS_OK;
+    }
+    throw EvalError("unknown option '" + k + "'");
+  });
+}
+
 int ps_geo_mean_rel_error(const double* pred, const double* meas, int n, double* out) {
   return guarded([&] {
     *out = geo_mean_rel_error(std::vector<double>(pred, pred + n), std::vector<double>(meas, meas + n));

@@ -131,6 +131,14 @@ class HostModel:
             return ops[: n_ops.value].copy(), consts[: n_consts.value].copy(), stack.value
 
 
+def set_option(key: str, value: str) -> None:
+    """ps_set_option, e.g. ("partial_subgroups", "round_up") for 18x18 tiles."""
+    L = _declare()
+    L.ps_set_option.argtypes = [C.c_char_p, C.c_char_p]
+    L.ps_set_option.restype = C.c_int
+    check(L.ps_set_option(key.encode(), value.encode()))
+
+
 def default_fit_opts() -> FitOpts:
     """FitOptions defaults (reference model.hpp:71-80)."""
     return FitOpts(1e-3, 0.1, 10.0, 1e-10, 1e-10, 200, 0)

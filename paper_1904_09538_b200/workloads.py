@@ -137,17 +137,24 @@ MATMUL = Workload(
     size_keys=("n",),
 )
 
-FD_GMEM = [("p_g16", G16), ("p_fd16u", _tag("fd-16x16-u")), ("p_fd16res", _tag("fd-16x16-res"))]
+G18 = "f_mem_access_global_float32_lstrides:{0:1;1:>1}_gstrides:{0:18;1:>18}_afr:1"
+FD_GMEM = [("p_g16", G16), ("p_g18", G18),
+           ("p_fd16u", _tag("fd-16x16-u")), ("p_fd16res", _tag("fd-16x16-res")),
+           ("p_fd18u", _tag("fd-18x18-u")), ("p_fd18res", _tag("fd-18x18-res"))]
 
 FD = Workload(
     name="fd",
-    description=("BASELINE.json configs[0]: five-point FD stencil, 16x16 tiles, grids "
-                 "1120^2..8176^2, linear model (PAPER.md:2560-2670)"),
-    calibration_tags=MICRO_TAGS + [["finite_diff_rm", "tile:16x16"]],
-    application_tags=[["finite_diff", "tile:16x16"]],
-    models={"linear": linear_model(FD_GMEM, ONCHIP)},
+    description=("BASELINE.json configs[0]: five-point FD stencil, 16x16 and 18x18 tiles, "
+                 "grids 1120^2..8176^2, calibrated from the microbenchmark sweep (gmem 16x16 and "
+                 "18x18 patterns) plus the fd-* work-removed kernels (PAPER.md:2560-2670); "
+                 "18x18 sub-group counts use the ceil(324/32) extension (SURVEY A1)"),
+    calibration_tags=MICRO_TAGS + [["gmem_pattern_18"], ["finite_diff_rm"]],
+    application_tags=[["finite_diff"]],
+    models={"linear": linear_model(FD_GMEM, ONCHIP),
+            "max3": max3_model(FD_GMEM, ONCHIP[:3], ONCHIP[3:])},
     variant_keys=("tile",),
     size_keys=("n",),
+    extra={"options": {"partial_subgroups": "round_up"}},
 )
 
 WORKLOADS = {w.name: w for w in (MATMUL, FD)}
