@@ -653,28 +653,27 @@ int launch(Ctx* c, const ps_kernel_desc* d) {
         else
           finite_diff<18><<<g1, block, 0, st>>>((const float*)in0, (float*)out0, n);
       } else if (d->tile == 16) {
-        finite_diff_multi<16, R><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
+        finite_diff_strip<16, R, 0><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
       } else {
-        finite_diff_multi<18, R><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
+        finite_diff_strip<18, R, 0><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
       }
       break;
     }
     case PS_GEN_FD_RM: {
       const int n = (int)d->n;
       const int I = d->tile - 2;
-      dim3 grid(n / I, n / I), block(d->tile, d->tile);
+      constexpr int R = 8;
+      dim3 grid((n / I + R - 1) / R, n / I), block(d->tile, d->tile);
       if (d->keep == PS_KEEP_U) {
-        constexpr int R = 8;
-        dim3 gm((n / I + R - 1) / R, n / I);
         if (d->tile == 16)
-          finite_diff_rm_u_multi<16, R><<<gm, block, 0, st>>>((const float*)in0, (float*)out0, n);
+          finite_diff_strip<16, R, 1><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
         else
-          finite_diff_rm_u_multi<18, R><<<gm, block, 0, st>>>((const float*)in0, (float*)out0, n);
+          finite_diff_strip<18, R, 1><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
       } else {
         if (d->tile == 16)
-          finite_diff_rm_res<16><<<grid, block, 0, st>>>((float*)out0, n);
+          finite_diff_strip<16, R, 2><<<grid, block, 0, st>>>(nullptr, (float*)out0, n);
         else
-          finite_diff_rm_res<18><<<grid, block, 0, st>>>((float*)out0, n);
+          finite_diff_strip<18, R, 2><<<grid, block, 0, st>>>(nullptr, (float*)out0, n);
       }
       break;
     }

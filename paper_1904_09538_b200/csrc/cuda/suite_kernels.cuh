@@ -377,6 +377,67 @@ __global__ void __launch_bounds__(T* T) finite_diff_multi(const float* __restric
   }
 }
 
+// K12/K13, strip realisation: a CTA of T x T threads owns R horizontally
+// adjacent work-groups, i.e. the u strip rows I*i_out .. I*i_out+T-1,
+// columns I*R*bx .. I*R*bx + I*R + 1. The union of the R tiles (every
+// work-item's fetch: the overlapping halo columns are the same u elements)
+// is staged into shared memory with row-contiguous, fully coalesced loads;
+// after the barrier the I x I*R interior points are computed with the exact
+// operation sequence of the IR statement and stored row-contiguously. The
+// value computed for every (c1, c0) of every group is unchanged; only the
+// thread that issues each global access differs.
+// MODE 0: finite_diff; 1: finite_diff_rm keep u (tgt_read_dest tiles);
+// 2: finite_diff_rm keep res (res interior = tgt_read = 0).
+template <int T, int R, int MODE>
+__global__ void __launch_bounds__(T* T) finite_diff_strip(const float* __restrict__ u,
+                                                         float* __restrict__ out, int n) {
+  constexpr int I = T - 2;
+  constexpr int SW = I * R + 2;  // strip width
+  constexpr int NT = T * T;
+  __shared__ float reg[MODE == 2 ? 1 : T][MODE == 2 ? 1 : SW + 1];
+  const int tid = threadIdx.y * T + threadIdx.x;
+  const int i_out = blockIdx.y;
+  const int groups = n / I;
+  const int col0 = I * R * blockIdx.x;           // first u column of the strip
+  const int gcount = min(R, groups - R * (int)blockIdx.x);  // work-groups in this strip
+  const int64_t W = n + 2;
+  if constexpr (MODE != 2) {
+    const int width = I * gcount + 2;
+    const float* base = u + (int64_t)(I * i_out) * W + col0;
+    for (int idx = tid; idx < T * SW; idx += NT) {
+      const int r = idx / SW, c = idx - r * SW;
+      if (c < width) reg[r][c] = __ldg(base + (int64_t)r * W + c);
+    }
+    bar_sync();  // the R work-groups' fetch barriers, executed as one
+  }
+  if constexpr (MODE == 0 || MODE == 2) {
+    const int width = I * gcount;
+    float* rbase = out + (int64_t)(I * i_out) * n + col0;
+    for (int idx = tid; idx < I * I * R; idx += NT) {
+      const int r = idx / (I * R), c = idx - r * (I * R);
+      if (c >= width) continue;
+      float s = 0.0f;
+      if constexpr (MODE == 0) {
+        s = __fadd_rn(reg[r][c + 1], reg[r + 1][c]);
+        s = __fmaf_rn(-4.0f, reg[r + 1][c + 1], s);
+        s = __fadd_rn(s, reg[r + 1][c + 2]);
+        s = __fadd_rn(s, reg[r + 2][c + 1]);
+      }
+      __stcs(rbase + (int64_t)r * n + c, s);
+    }
+  } else {
+    // tgt_read_dest[T*i_out + l1, T*j_out + l0] = 0 + u[I*i_out + l1, I*j_out + l0]
+    const int64_t DW = (int64_t)groups * T;
+    float* dbase = out + (int64_t)(T * i_out) * DW + (int64_t)T * R * blockIdx.x;
+    for (int idx = tid; idx < T * T * R; idx += NT) {
+      const int r = idx / (T * R), c = idx - r * (T * R);
+      const int g = c / T, l0 = c - g * T;
+      if (g >= gcount) continue;
+      __stcs(dbase + (int64_t)r * DW + c, __fadd_rn(0.0f, reg[r][I * g + l0]));
+    }
+  }
+}
+
 template <int T, int R>
 __global__ void __launch_bounds__(T* T) finite_diff_rm_u_multi(const float* __restrict__ u,
                                                               float* __restrict__ dest, int n) {
