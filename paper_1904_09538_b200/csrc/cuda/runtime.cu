@@ -643,37 +643,59 @@ int launch(Ctx* c, const ps_kernel_desc* d) {
     case PS_GEN_FD: {
       const int n = (int)d->n;
       const int I = d->tile - 2;
-      constexpr int R = 8;
       const int groups = n / I;
-      dim3 grid((groups + R - 1) / R, groups), block(d->tile, d->tile);
+      dim3 block(d->tile, d->tile);
+      dim3 sblock(FD_STRIP_THREADS);
+      // widest strip that still leaves >= 8 CTAs per SM to schedule (wide
+      // strips keep more loads in flight per thread; narrow ones fill the
+      // 148 SMs on small grids)
+      const int64_t want = 8LL * c->sm_count;
+      const int R = ((int64_t)(groups + 31) / 32 * groups >= want)   ? 32
+                    : ((int64_t)(groups + 15) / 16 * groups >= want) ? 16
+                                                                      : 8;
+      dim3 grid((groups + R - 1) / R, groups);
       if (c->force_generic) {
         dim3 g1(groups, groups);
         if (d->tile == 16)
           finite_diff<16><<<g1, block, 0, st>>>((const float*)in0, (float*)out0, n);
         else
           finite_diff<18><<<g1, block, 0, st>>>((const float*)in0, (float*)out0, n);
-      } else if (d->tile == 16) {
-        finite_diff_strip<16, R, 0><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
       } else {
-        finite_diff_strip<18, R, 0><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
+#define PS_FD_STRIP(TT, RR) \
+  finite_diff_strip<TT, RR, 0><<<grid, sblock, 0, st>>>((const float*)in0, (float*)out0, n)
+        if (d->tile == 16) {
+          if (R == 32) PS_FD_STRIP(16, 32); else if (R == 16) PS_FD_STRIP(16, 16); else PS_FD_STRIP(16, 8);
+        } else {
+          if (R == 32) PS_FD_STRIP(18, 32); else if (R == 16) PS_FD_STRIP(18, 16); else PS_FD_STRIP(18, 8);
+        }
+#undef PS_FD_STRIP
       }
       break;
     }
     case PS_GEN_FD_RM: {
       const int n = (int)d->n;
       const int I = d->tile - 2;
-      constexpr int R = 8;
-      dim3 grid((n / I + R - 1) / R, n / I), block(d->tile, d->tile);
+      const int groups = n / I;
+      const int64_t want = 8LL * c->sm_count;
+      const int R = (d->keep == PS_KEEP_U && (int64_t)(groups + 15) / 16 * groups >= want) ? 16 : 8;
+      dim3 grid((groups + R - 1) / R, groups), block(FD_STRIP_THREADS);
       if (d->keep == PS_KEEP_U) {
-        if (d->tile == 16)
-          finite_diff_strip<16, R, 1><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
-        else
-          finite_diff_strip<18, R, 1><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
+        if (d->tile == 16) {
+          if (R == 16)
+            finite_diff_strip<16, 16, 1><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
+          else
+            finite_diff_strip<16, 8, 1><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
+        } else {
+          if (R == 16)
+            finite_diff_strip<18, 16, 1><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
+          else
+            finite_diff_strip<18, 8, 1><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);
+        }
       } else {
         if (d->tile == 16)
-          finite_diff_strip<16, R, 2><<<grid, block, 0, st>>>(nullptr, (float*)out0, n);
+          finite_diff_strip<16, 8, 2><<<grid, block, 0, st>>>(nullptr, (float*)out0, n);
         else
-          finite_diff_strip<18, R, 2><<<grid, block, 0, st>>>(nullptr, (float*)out0, n);
+          finite_diff_strip<18, 8, 2><<<grid, block, 0, st>>>(nullptr, (float*)out0, n);
       }
       break;
     }

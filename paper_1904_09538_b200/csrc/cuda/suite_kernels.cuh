@@ -377,63 +377,132 @@ __global__ void __launch_bounds__(T* T) finite_diff_multi(const float* __restric
   }
 }
 
-// K12/K13, strip realisation: a CTA of T x T threads owns R horizontally
-// adjacent work-groups, i.e. the u strip rows I*i_out .. I*i_out+T-1,
-// columns I*R*bx .. I*R*bx + I*R + 1. The union of the R tiles (every
-// work-item's fetch: the overlapping halo columns are the same u elements)
-// is staged into shared memory with row-contiguous, fully coalesced loads;
-// after the barrier the I x I*R interior points are computed with the exact
-// operation sequence of the IR statement and stored row-contiguously. The
-// value computed for every (c1, c0) of every group is unchanged; only the
-// thread that issues each global access differs.
+// K12/K13, strip realisation: one CTA of FD_STRIP_THREADS threads owns R
+// horizontally adjacent work-groups, i.e. the u strip rows I*i_out ..
+// I*i_out+T-1, columns I*R*bx .. I*R*bx + I*R + 1. The union of the R tiles
+// (every work-item's fetch: the overlapping halo columns are the same u
+// elements) is staged into shared memory warp-per-row with coalesced loads,
+// all of a thread's loads in flight before its first shared store; after the
+// barrier the I x I*R interior points are computed with the exact operation
+// sequence of the IR statement and stored warp-per-row (16-byte stores when
+// rows are 16-byte aligned). The value computed for every (c1, c0) of every
+// group is unchanged; only the thread that issues each access differs, and
+// the CTA shape no longer follows the T x T work-group (a 324-thread 18x18
+// group is not a whole number of warps).
 // MODE 0: finite_diff; 1: finite_diff_rm keep u (tgt_read_dest tiles);
 // 2: finite_diff_rm keep res (res interior = tgt_read = 0).
+constexpr int FD_STRIP_THREADS = 256;
+
 template <int T, int R, int MODE>
-__global__ void __launch_bounds__(T* T) finite_diff_strip(const float* __restrict__ u,
-                                                         float* __restrict__ out, int n) {
+__global__ void __launch_bounds__(FD_STRIP_THREADS) finite_diff_strip(const float* __restrict__ u,
+                                                                     float* __restrict__ out, int n) {
   constexpr int I = T - 2;
-  constexpr int SW = I * R + 2;  // strip width
-  constexpr int NT = T * T;
-  __shared__ float reg[MODE == 2 ? 1 : T][MODE == 2 ? 1 : SW + 1];
-  const int tid = threadIdx.y * T + threadIdx.x;
+  constexpr int SW = I * R + 2;             // strip width
+  constexpr int NW = FD_STRIP_THREADS / 32;  // warps
+  constexpr int CJ = (SW + 31) / 32;         // 32-column chunks per strip row
+  constexpr int RW = (T + NW - 1) / NW;      // strip rows per warp (upper bound)
+  // row pitch: a multiple of 4 floats so that every strip row starts 16-byte
+  // aligned and the stencil reads its rows with conflict-free LDS.128
+  constexpr int P = CJ * 32 + 4;
+  __shared__ __align__(16) float reg[MODE == 2 ? 1 : T][MODE == 2 ? 4 : P];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i_out = blockIdx.y;
   const int groups = n / I;
-  const int col0 = I * R * blockIdx.x;           // first u column of the strip
+  const int col0 = I * R * blockIdx.x;                      // first u column of the strip
   const int gcount = min(R, groups - R * (int)blockIdx.x);  // work-groups in this strip
   const int64_t W = n + 2;
   if constexpr (MODE != 2) {
     const int width = I * gcount + 2;
-    const float* base = u + (int64_t)(I * i_out) * W + col0;
-    for (int idx = tid; idx < T * SW; idx += NT) {
-      const int r = idx / SW, c = idx - r * SW;
-      if (c < width) reg[r][c] = __ldg(base + (int64_t)r * W + c);
+    const float* base = u + (int64_t)(I * i_out) * W + col0 + lane;
+    float v[RW][CJ];
+#pragma unroll
+    for (int k = 0; k < RW; ++k) {
+      const int r = warp + k * NW;
+      const float* row = base + (int64_t)r * W;
+#pragma unroll
+      for (int j = 0; j < CJ; ++j)
+        v[k][j] = (r < T && lane + 32 * j < width) ? __ldg(row + 32 * j) : 0.0f;
+    }
+#pragma unroll
+    for (int k = 0; k < RW; ++k) {
+      const int r = warp + k * NW;
+      if (r < T) {
+#pragma unroll
+        for (int j = 0; j < CJ; ++j) reg[r][lane + 32 * j] = v[k][j];
+      }
     }
     bar_sync();  // the R work-groups' fetch barriers, executed as one
   }
   if constexpr (MODE == 0 || MODE == 2) {
     const int width = I * gcount;
     float* rbase = out + (int64_t)(I * i_out) * n + col0;
-    for (int idx = tid; idx < I * I * R; idx += NT) {
-      const int r = idx / (I * R), c = idx - r * (I * R);
-      if (c >= width) continue;
-      float s = 0.0f;
-      if constexpr (MODE == 0) {
-        s = __fadd_rn(reg[r][c + 1], reg[r + 1][c]);
-        s = __fmaf_rn(-4.0f, reg[r + 1][c + 1], s);
-        s = __fadd_rn(s, reg[r + 1][c + 2]);
-        s = __fadd_rn(s, reg[r + 2][c + 1]);
+    if ((n & 3) == 0) {  // rows and strip offsets are 16-byte aligned
+      static_assert((I * R) % 4 == 0, "strip row must hold whole float4");
+      constexpr int Q = I * R / 4;  // float4 per output row
+      constexpr int QJ = (Q + 31) / 32;
+      for (int r = warp; r < I; r += NW) {
+#pragma unroll
+        for (int j = 0; j < QJ; ++j) {
+          const int c = 4 * (lane + 32 * j);
+          if (c >= width) continue;
+          float o[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          if constexpr (MODE == 0) {
+            // rows r, r+1, r+2 over columns c .. c+7 (two aligned float4 each)
+            const float4* q0 = reinterpret_cast<const float4*>(&reg[r][c]);
+            const float4* q1 = reinterpret_cast<const float4*>(&reg[r + 1][c]);
+            const float4* q2 = reinterpret_cast<const float4*>(&reg[r + 2][c]);
+            const float4 a0 = q0[0], b0 = q0[1], a1 = q1[0], b1 = q1[1], a2 = q2[0], b2 = q2[1];
+            const float x0[4] = {a0.y, a0.z, a0.w, b0.x};
+            const float x1[6] = {a1.x, a1.y, a1.z, a1.w, b1.x, b1.y};
+            const float x2[4] = {a2.y, a2.z, a2.w, b2.x};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              float t = __fadd_rn(x0[k], x1[k]);
+              t = __fmaf_rn(-4.0f, x1[k + 1], t);
+              t = __fadd_rn(t, x1[k + 2]);
+              o[k] = __fadd_rn(t, x2[k]);
+            }
+          }
+          float* dst = rbase + (int64_t)r * n + c;
+          if (c + 3 < width) {
+            __stcs(reinterpret_cast<float4*>(dst), make_float4(o[0], o[1], o[2], o[3]));
+          } else {
+            for (int q = 0; q < 4 && c + q < width; ++q) __stcs(dst + q, o[q]);
+          }
+        }
       }
-      __stcs(rbase + (int64_t)r * n + c, s);
+    } else {
+      constexpr int QJ = (I * R + 31) / 32;
+      for (int r = warp; r < I; r += NW) {
+#pragma unroll
+        for (int j = 0; j < QJ; ++j) {
+          const int c = lane + 32 * j;
+          if (c >= width) continue;
+          float s = 0.0f;
+          if constexpr (MODE == 0) {
+            s = __fadd_rn(reg[r][c + 1], reg[r + 1][c]);
+            s = __fmaf_rn(-4.0f, reg[r + 1][c + 1], s);
+            s = __fadd_rn(s, reg[r + 1][c + 2]);
+            s = __fadd_rn(s, reg[r + 2][c + 1]);
+          }
+          __stcs(rbase + (int64_t)r * n + c, s);
+        }
+      }
     }
   } else {
     // tgt_read_dest[T*i_out + l1, T*j_out + l0] = 0 + u[I*i_out + l1, I*j_out + l0]
     const int64_t DW = (int64_t)groups * T;
+    const int width = T * gcount;
     float* dbase = out + (int64_t)(T * i_out) * DW + (int64_t)T * R * blockIdx.x;
-    for (int idx = tid; idx < T * T * R; idx += NT) {
-      const int r = idx / (T * R), c = idx - r * (T * R);
-      const int g = c / T, l0 = c - g * T;
-      if (g >= gcount) continue;
-      __stcs(dbase + (int64_t)r * DW + c, __fadd_rn(0.0f, reg[r][I * g + l0]));
+    constexpr int DJ = (T * R + 31) / 32;
+    for (int r = warp; r < T; r += NW) {
+#pragma unroll
+      for (int j = 0; j < DJ; ++j) {
+        const int c = lane + 32 * j;
+        if (c >= width) continue;
+        const int g = c / T, l0 = c - g * T;
+        __stcs(dbase + (int64_t)r * DW + c, __fadd_rn(0.0f, reg[r][I * g + l0]));
+      }
     }
   }
 }

@@ -42,7 +42,9 @@ for dt in ("float32", "float64"):
             for keep in ("a", "b"):
                 CASES.append(vid("matmul_sq_rm", dtype=dt, prefetch=pf, keep=keep, lsize_0=16,
                                  lsize_1=16, groups_fit="True", n=n))
-for tile, ns in (("16x16", (14, 28, 112)), ("18x18", (16, 48, 112))):
+# 1960/2400 and 2744/3200 select the 16- and 32-group strip launches (with a
+# partial last strip); n = 14 exercises the unaligned (n % 4 != 0) store path
+for tile, ns in (("16x16", (14, 28, 112, 1960, 2744)), ("18x18", (16, 48, 112, 2400, 3200))):
     for n in ns:
         CASES.append(vid("finite_diff", dtype="float32", tile=tile, n=n))
         for keep in ("u", "res"):
