@@ -30,29 +30,42 @@ __device__ __forceinline__ int64_t dg_res_idx(bool trans, const DgDims& d, int m
   return trans ? ((int64_t)m * d.np + i) * d.nel + k : ((int64_t)m * d.nel + k) * d.np + i;
 }
 
-// noPF: no local memory; m outermost, reduction over j.
+// noPF: no local memory; m outermost, reduction over j. The work-item's own
+// row reads along the sequential j are issued as 16-byte loads (Np is a
+// multiple of 16, so rows are 64-byte aligned): the same thread reads the same
+// elements and accumulates them in the same order, in a quarter of the load
+// instructions (each warp-wide u load touches 16 rows either way).
 __global__ void __launch_bounds__(256) dg_nopf(const float* __restrict__ dm,
                                                const float* __restrict__ u,
                                                float* __restrict__ res, DgDims d) {
   const int64_t k = (int64_t)blockIdx.x * 16 + threadIdx.x;
   const int i = blockIdx.y * 16 + threadIdx.y;
+  const float4* urow = reinterpret_cast<const float4*>(u + k * d.np);
   for (int m = 0; m < d.nmat; ++m) {
-    const float* dmrow = dm + ((int64_t)m * d.np + i) * d.np;
-    const float* urow = u + k * d.np;
+    const float4* dmrow = reinterpret_cast<const float4*>(dm + ((int64_t)m * d.np + i) * d.np);
     float acc = 0.f;
-#pragma unroll 8
-    for (int j = 0; j < d.np; ++j) acc = __fmaf_rn(dmrow[j], urow[j], acc);
+#pragma unroll 4
+    for (int j4 = 0; j4 < d.np / 4; ++j4) {
+      const float4 a = __ldg(dmrow + j4), b = __ldg(urow + j4);
+      acc = __fmaf_rn(a.x, b.x, acc);
+      acc = __fmaf_rn(a.y, b.y, acc);
+      acc = __fmaf_rn(a.z, b.z, acc);
+      acc = __fmaf_rn(a.w, b.w, acc);
+    }
     res[dg_res_idx(false, d, m, k, i)] = acc;
   }
 }
 
 // uPF: 16x16 tiles of u staged in shared memory per j_out (two barriers per
 // tile), m privatised into NMAT accumulators, loop order j_out, j_in, m.
+// Row pitch 20 keeps u_fetch rows 16-byte aligned (conflict-free LDS.128 per
+// quarter warp); the work-item's dm row and u_fetch row are read 4 j_in at a
+// time, the FMAs still run in j_in, m order.
 template <int NMAT>
 __global__ void __launch_bounds__(256) dg_upf(const float* __restrict__ dm,
                                               const float* __restrict__ u,
                                               float* __restrict__ res, DgDims d) {
-  __shared__ float uf[16][17];
+  __shared__ __align__(16) float uf[16][20];
   const int lx = threadIdx.x, ly = threadIdx.y;
   const int64_t k0 = (int64_t)blockIdx.x * 16;
   const int i = blockIdx.y * 16 + ly;
@@ -64,11 +77,21 @@ __global__ void __launch_bounds__(256) dg_upf(const float* __restrict__ dm,
     uf[ly][lx] = u[(k0 + ly) * d.np + jo * 16 + lx];  // u_fetch[k_in, j_in], j_in -> l.0
     bar_sync();
 #pragma unroll
-    for (int ji = 0; ji < 16; ++ji) {
-      const float uv = uf[lx][ji];
+    for (int j4 = 0; j4 < 4; ++j4) {
+      const float4 uv = *reinterpret_cast<const float4*>(&uf[lx][4 * j4]);
+      float4 dv[NMAT];
 #pragma unroll
       for (int m = 0; m < NMAT; ++m)
-        acc[m] = __fmaf_rn(dm[((int64_t)m * d.np + i) * d.np + jo * 16 + ji], uv, acc[m]);
+        dv[m] = __ldg(reinterpret_cast<const float4*>(dm + ((int64_t)m * d.np + i) * d.np +
+                                                      jo * 16 + 4 * j4));
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m) acc[m] = __fmaf_rn(dv[m].x, uv.x, acc[m]);
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m) acc[m] = __fmaf_rn(dv[m].y, uv.y, acc[m]);
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m) acc[m] = __fmaf_rn(dv[m].z, uv.z, acc[m]);
+#pragma unroll
+      for (int m = 0; m < NMAT; ++m) acc[m] = __fmaf_rn(dv[m].w, uv.w, acc[m]);
     }
   }
 #pragma unroll
@@ -77,12 +100,14 @@ __global__ void __launch_bounds__(256) dg_upf(const float* __restrict__ dm,
 
 // dmPF / dmPFtrans: per m and j_out, a 16x16 tile of dm staged in shared
 // memory (two barriers per tile); u read directly (strided by Np in dmPF,
-// unit-stride across lid(0) in the transposed layout).
+// unit-stride across lid(0) in the transposed layout). The work-item's
+// dm_fetch row is read 4 j_in at a time (LDS.128, pitch 20), and in dmPF its
+// u row too (LDG.128); FMAs in j_in order.
 template <bool TRANS>
 __global__ void __launch_bounds__(256) dg_dmpf(const float* __restrict__ dm,
                                                const float* __restrict__ u,
                                                float* __restrict__ res, DgDims d) {
-  __shared__ float dmf[16][17];
+  __shared__ __align__(16) float dmf[16][20];
   const int lx = threadIdx.x, ly = threadIdx.y;
   const int64_t k = (int64_t)blockIdx.x * 16 + lx;
   const int i0 = blockIdx.y * 16;
@@ -93,8 +118,23 @@ __global__ void __launch_bounds__(256) dg_dmpf(const float* __restrict__ dm,
       dmf[ly][lx] = dm[((int64_t)m * d.np + i0 + ly) * d.np + jo * 16 + lx];
       bar_sync();
 #pragma unroll
-      for (int ji = 0; ji < 16; ++ji)
-        acc = __fmaf_rn(dmf[ly][ji], u[dg_u_idx(TRANS, d, k, jo * 16 + ji)], acc);
+      for (int j4 = 0; j4 < 4; ++j4) {
+        const float4 a = *reinterpret_cast<const float4*>(&dmf[ly][4 * j4]);
+        float4 b;
+        if constexpr (TRANS) {
+          const int j = jo * 16 + 4 * j4;
+          b.x = __ldg(u + (int64_t)j * d.nel + k);
+          b.y = __ldg(u + (int64_t)(j + 1) * d.nel + k);
+          b.z = __ldg(u + (int64_t)(j + 2) * d.nel + k);
+          b.w = __ldg(u + (int64_t)(j + 3) * d.nel + k);
+        } else {
+          b = __ldg(reinterpret_cast<const float4*>(u + k * d.np + jo * 16 + 4 * j4));
+        }
+        acc = __fmaf_rn(a.x, b.x, acc);
+        acc = __fmaf_rn(a.y, b.y, acc);
+        acc = __fmaf_rn(a.z, b.z, acc);
+        acc = __fmaf_rn(a.w, b.w, acc);
+      }
     }
     res[dg_res_idx(TRANS, d, m, k, i0 + ly)] = acc;
   }
@@ -120,28 +160,62 @@ __global__ void __launch_bounds__(256) dg_rm(const float* __restrict__ src,
   } else {
     float acc = 0.f;
     const int njo = d.np / 16;
+    // row reads along the sequential j use the same 16-byte loads as the
+    // application kernels (same accesses, same fadd order)
+    auto add4 = [&](float4 v) {
+      acc = __fadd_rn(acc, v.x);
+      acc = __fadd_rn(acc, v.y);
+      acc = __fadd_rn(acc, v.z);
+      acc = __fadd_rn(acc, v.w);
+    };
     if constexpr (VARIANT == 0) {
       // statement within (m, k, i), reduction j
-      for (int m = 0; m < d.nmat; ++m)
-        for (int j = 0; j < d.np; ++j)
-          acc = __fadd_rn(acc, KEEP == 3 ? src[k * d.np + j]
-                                         : src[((int64_t)m * d.np + i) * d.np + j]);
+      for (int m = 0; m < d.nmat; ++m) {
+        const float4* row = reinterpret_cast<const float4*>(
+            KEEP == 3 ? src + k * d.np : src + ((int64_t)m * d.np + i) * d.np);
+#pragma unroll 4
+        for (int j4 = 0; j4 < d.np / 4; ++j4) add4(__ldg(row + j4));
+      }
     } else if constexpr (VARIANT == 1) {
       if constexpr (KEEP == 3) {
         // fetch: one u load per (work-item, j_out)
         for (int jo = 0; jo < njo; ++jo) acc = __fadd_rn(acc, src[(k0 + ly) * d.np + jo * 16 + lx]);
       } else {
-        for (int jo = 0; jo < njo; ++jo)
-          for (int ji = 0; ji < 16; ++ji)
-            for (int m = 0; m < d.nmat; ++m)
-              acc = __fadd_rn(acc, src[((int64_t)m * d.np + i) * d.np + jo * 16 + ji]);
+        // the uPF update's dm reads: per j_out, 4 x nmat row quads in flight
+        for (int jo = 0; jo < njo; ++jo) {
+          float4 v[4][4];
+#pragma unroll
+          for (int j4 = 0; j4 < 4; ++j4)
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              if (m < d.nmat)
+                v[j4][m] = __ldg(reinterpret_cast<const float4*>(
+                    src + ((int64_t)m * d.np + i) * d.np + jo * 16 + 4 * j4));
+#pragma unroll
+          for (int j4 = 0; j4 < 4; ++j4) {
+#pragma unroll
+            for (int m = 0; m < 4; ++m) if (m < d.nmat) acc = __fadd_rn(acc, v[j4][m].x);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) if (m < d.nmat) acc = __fadd_rn(acc, v[j4][m].y);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) if (m < d.nmat) acc = __fadd_rn(acc, v[j4][m].z);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) if (m < d.nmat) acc = __fadd_rn(acc, v[j4][m].w);
+          }
+        }
       }
     } else {
       if constexpr (KEEP == 3) {
         for (int m = 0; m < d.nmat; ++m)
           for (int jo = 0; jo < njo; ++jo)
-            for (int ji = 0; ji < 16; ++ji)
-              acc = __fadd_rn(acc, src[dg_u_idx(TRANS, d, k, jo * 16 + ji)]);
+            for (int j4 = 0; j4 < 4; ++j4) {
+              const int j = jo * 16 + 4 * j4;
+              if constexpr (TRANS) {
+                for (int q = 0; q < 4; ++q) acc = __fadd_rn(acc, src[dg_u_idx(true, d, k, j + q)]);
+              } else {
+                add4(__ldg(reinterpret_cast<const float4*>(src + k * d.np + j)));
+              }
+            }
       } else {
         for (int m = 0; m < d.nmat; ++m)
           for (int jo = 0; jo < njo; ++jo)

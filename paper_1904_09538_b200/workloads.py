@@ -81,6 +81,19 @@ def max3_model(gmem: list[tuple[str, str]], ops: list[tuple[str, str]],
     return OUTPUT + "\n" + ovh + " + " + sharp_max(cg, onchip, k) + "\n"
 
 
+def lsu_model(gmem: list[tuple[str, str]], ops: list[tuple[str, str]],
+              lmem: list[tuple[str, str]], k: float = 40.0) -> str:
+    """launch/group overhead + max(c_gmem + c_lmem, c_ops, c_barrier): on
+    sm_100 global loads that hit L1 and shared-memory accesses are issued
+    through the same LSU/MIO pipe and do not overlap each other; either
+    overlaps the FP32 pipe."""
+    ovh = _sum([f"p_group * {GROUPS}", f"p_launch * {LAUNCH}"])
+    cmem = _sum([f"{p} * {f}" for p, f in gmem] + [f"{p} * {f}" for p, f in lmem])
+    cops = _sum([f"{p} * {f}" for p, f in ops])
+    cb = f"p_bar * {BAR} * {GROUPS}"
+    return OUTPUT + "\n" + ovh + " + " + sharp_max(cmem, sharp_max(cops, cb, k), k) + "\n"
+
+
 def overlap3_model(gmem: list[tuple[str, str]], ops: list[tuple[str, str]],
                    lmem: list[tuple[str, str]]) -> str:
     """ovh + max(c_gmem, max(c_ops, c_lmem)): the paper's overlap form with the
@@ -117,6 +130,8 @@ class Workload:
     size_keys: tuple[str, ...] = ("n",)
     hbm_generators: tuple[str, ...] = ("gmem_pattern", "overlap_knl")
     extra: dict = field(default_factory=dict)
+    # model whose GPU fit is the bench headline: the B200 LSU/FMA overlap model
+    headline_model: str = "lsu"
 
 
 MATMUL_GMEM = [("p_g16", G16), ("p_mmPFa", _tag("mm-PF-a")), ("p_mmPFb", _tag("mm-PF-b")),
@@ -132,7 +147,8 @@ MATMUL = Workload(
     models={"linear": linear_model(MATMUL_GMEM, ONCHIP),
             "nonlinear": overlap_model(MATMUL_GMEM, ONCHIP),
             "overlap3": overlap3_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:]),
-            "max3": max3_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:])},
+            "max3": max3_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:]),
+            "lsu": lsu_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:])},
     variant_keys=("prefetch",),
     size_keys=("n",),
 )
@@ -151,13 +167,42 @@ FD = Workload(
     calibration_tags=MICRO_TAGS + [["gmem_pattern_18"], ["finite_diff_rm"]],
     application_tags=[["finite_diff"]],
     models={"linear": linear_model(FD_GMEM, ONCHIP),
-            "max3": max3_model(FD_GMEM, ONCHIP[:3], ONCHIP[3:])},
+            "max3": max3_model(FD_GMEM, ONCHIP[:3], ONCHIP[3:]),
+            "lsu": lsu_model(FD_GMEM, ONCHIP[:3], ONCHIP[3:])},
     variant_keys=("tile",),
     size_keys=("n",),
     extra={"options": {"partial_subgroups": "round_up"}},
 )
 
-WORKLOADS = {w.name: w for w in (MATMUL, FD)}
+DG_TAGS = ["dg-noPF-u", "dg-noPF-res", "dg-uPFnoPF-dm", "dg-uPF-u", "dg-uPF-res", "dg-dmPF-dm",
+           "dg-dmPF-u", "dg-dmPF-res", "dg-dmPFtrans-u", "dg-dmPFtrans-res"]
+DG_GMEM = [("p_g16", G16)] + [("p_" + t.replace("-", "_"), _tag(t)) for t in DG_TAGS]
+
+DG = Workload(
+    name="dg",
+    description=("BASELINE.json configs[2]: DG differentiation res[m,k,i] = sum_j dm[m,i,j] u[k,j], "
+                 "4 variants (noPF, uPF, dmPF, dmPFtrans), nmat=3, Np=64, nel 10^4..10^6, "
+                 "calibrated from the microbenchmark sweep plus the 10 dg-* work-removed tags "
+                 "(PAPER.md:2041-2050, 2354-2505)"),
+    calibration_tags=MICRO_TAGS + [["dg_diff_rm"]],
+    application_tags=[["dg_diff"]],
+    models={"linear": linear_model(DG_GMEM, ONCHIP),
+            "max3": max3_model(DG_GMEM, ONCHIP[:3], ONCHIP[3:]),
+            "lsu": lsu_model(DG_GMEM, ONCHIP[:3], ONCHIP[3:])},
+    variant_keys=("variant",),
+    size_keys=("nelements",),
+)
+
+WORKLOADS = {w.name: w for w in (MATMUL, FD, DG)}
+# "all": one calibration sweep over the union of the three workloads' kernels
+# (BASELINE.json configs[3]); every workload's models are fitted on its own rows
+GROUPS = {"all": ["matmul", "fd", "dg"]}
+
+
+def resolve(name: str) -> list[Workload]:
+    if name in GROUPS:
+        return [WORKLOADS[n] for n in GROUPS[name]]
+    return [WORKLOADS[name]]
 
 
 def variant_of(variant_id: str, keys: tuple[str, ...]) -> str:

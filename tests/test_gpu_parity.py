@@ -56,6 +56,9 @@ for variant in ("noPF", "uPF", "dmPF", "dmPFtrans"):
         for keep in ("u", "dm", "res"):
             CASES.append(vid("dg_diff_rm", dtype="float32", variant=variant, keep=keep,
                              nelements=nel, nunit_nodes=np_, nmatrices=3))
+    # a bench-sized element count (625 k-groups) at the paper's Np = 64
+    CASES.append(vid("dg_diff", dtype="float32", variant=variant, nelements=10000,
+                     nunit_nodes=64, nmatrices=3))
 
 
 @pytest.fixture(scope="module")

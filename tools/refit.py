@@ -14,15 +14,17 @@ from paper_1904_09538_b200 import host  # noqa: E402
 table = sys.argv[1]
 wname = next((a for a in sys.argv[2:] if not a.startswith("--")), "matmul")
 rows = {r["kernel"]: float(r["mean_seconds"]) for r in csv.DictReader(open(table))}
-wl, cal, app = bench.workload_kernels(wname)
-cal = [k for k in cal if k in rows]
-app = [k for k in app if k in rows]
+parts, _ = bench.workload_kernels(wname)
 dev = None
 if "--gpu" in sys.argv:
     from paper_1904_09538_b200.device import CudaDevice
     dev = CudaDevice(0)
-print(json.dumps(bench.model_report(wl, cal, app, rows, dev), indent=1))
-if "--rows" in sys.argv:
+for wl, cal, app in parts:
+    cal = [k for k in cal if k in rows]
+    app = [k for k in app if k in rows]
+    print(wl.name, json.dumps(bench.model_report(wl, cal, app, rows, dev), indent=1))
+    if "--rows" not in sys.argv:
+        continue
     for mname, text in wl.models.items():
         m = host.HostModel(text)
         tc = np.array([rows[k] for k in cal])
