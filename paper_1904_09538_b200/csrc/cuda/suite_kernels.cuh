@@ -252,8 +252,33 @@ __global__ void __launch_bounds__(256) matmul_nopf(const T* __restrict__ a,
   const T* arow = a + (int64_t)i * n;
   const T* bcol = b + j;
   T acc = T(0);
+  if constexpr (sizeof(T) == 4) {
+    // the work-item's a row along the sequential k as 16-byte loads (n is a
+    // multiple of 16): same elements, same madd order, a quarter of the a
+    // load instructions
+    // All 10 loads of an 8-k step are issued before its first FMA (the madd
+    // chain is serial, so the loads are the only parallelism there is).
+    const float4* arow4 = reinterpret_cast<const float4*>(arow);
+    const int64_t n64 = n;
+    for (int k8 = 0; k8 < n / 8; ++k8) {
+      const float4 a0 = __ldg(arow4 + 2 * k8), a1 = __ldg(arow4 + 2 * k8 + 1);
+      const float* bk = bcol + 8 * (int64_t)k8 * n64;
+      float bv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) bv[q] = __ldg(bk + q * n64);
+      acc = fma_t(a0.x, bv[0], acc);
+      acc = fma_t(a0.y, bv[1], acc);
+      acc = fma_t(a0.z, bv[2], acc);
+      acc = fma_t(a0.w, bv[3], acc);
+      acc = fma_t(a1.x, bv[4], acc);
+      acc = fma_t(a1.y, bv[5], acc);
+      acc = fma_t(a1.z, bv[6], acc);
+      acc = fma_t(a1.w, bv[7], acc);
+    }
+  } else {
 #pragma unroll 8
-  for (int k = 0; k < n; ++k) acc = fma_t(arow[k], bcol[(int64_t)k * n], acc);
+    for (int k = 0; k < n; ++k) acc = fma_t(arow[k], bcol[(int64_t)k * n], acc);
+  }
   c[(int64_t)i * n + j] = acc;
 }
 
@@ -264,7 +289,7 @@ template <typename T, int TS>
 __global__ void __launch_bounds__(TS* TS) matmul_pf(const T* __restrict__ a,
                                                     const T* __restrict__ b, T* __restrict__ c,
                                                     int n) {
-  __shared__ T af[TS][TS];
+  __shared__ __align__(16) T af[TS][TS];
   __shared__ T bf[TS][TS];
   const int ti = threadIdx.y, tj = threadIdx.x;
   const int row = blockIdx.y * TS + ti;
@@ -276,8 +301,20 @@ __global__ void __launch_bounds__(TS* TS) matmul_pf(const T* __restrict__ a,
     af[ti][tj] = a[(int64_t)row * n + kt * TS + tj];
     bf[ti][tj] = b[(int64_t)(kt * TS + ti) * n + col];
     bar_sync();  // bar_post
+    if constexpr (sizeof(T) == 4 && TS % 4 == 0) {
+      // a_fetch row read 4 k_in at a time (LDS.128, a broadcast per half-warp)
 #pragma unroll
-    for (int kin = 0; kin < TS; ++kin) acc = fma_t(af[ti][kin], bf[kin][tj], acc);
+      for (int k4 = 0; k4 < TS / 4; ++k4) {
+        const float4 av = *reinterpret_cast<const float4*>(&af[ti][4 * k4]);
+        acc = fma_t(av.x, bf[4 * k4][tj], acc);
+        acc = fma_t(av.y, bf[4 * k4 + 1][tj], acc);
+        acc = fma_t(av.z, bf[4 * k4 + 2][tj], acc);
+        acc = fma_t(av.w, bf[4 * k4 + 3][tj], acc);
+      }
+    } else {
+#pragma unroll
+      for (int kin = 0; kin < TS; ++kin) acc = fma_t(af[ti][kin], bf[kin][tj], acc);
+    }
   }
   c[(int64_t)row * n + col] = acc;
 }
@@ -301,14 +338,35 @@ __global__ void __launch_bounds__(256) matmul_rm(const T* __restrict__ src,
       else
         acc = add_t(acc, src[(int64_t)(kt * tile + ti) * n + col]);
     }
+  } else if constexpr (KEEP == 1 && sizeof(T) == 4) {
+    // the application kernel's 16-byte a-row loads
+    const float4* row4 = reinterpret_cast<const float4*>(src + (int64_t)row * n);
+    for (int k8 = 0; k8 < n / 8; ++k8) {
+      const float4 v0 = __ldg(row4 + 2 * k8), v1 = __ldg(row4 + 2 * k8 + 1);
+      acc = add_t(acc, v0.x);
+      acc = add_t(acc, v0.y);
+      acc = add_t(acc, v0.z);
+      acc = add_t(acc, v0.w);
+      acc = add_t(acc, v1.x);
+      acc = add_t(acc, v1.y);
+      acc = add_t(acc, v1.z);
+      acc = add_t(acc, v1.w);
+    }
+  } else if constexpr (KEEP == 2) {
+    // b column, 8 loads in flight ahead of the serial add chain (as the
+    // application kernel issues them)
+    const T* bcol = src + col;
+    const int64_t n64 = n;
+    for (int k8 = 0; k8 < n / 8; ++k8) {
+      T v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __ldg(bcol + (8 * (int64_t)k8 + q) * n64);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc = add_t(acc, v[q]);
+    }
   } else {
 #pragma unroll 8
-    for (int k = 0; k < n; ++k) {
-      if constexpr (KEEP == 1)
-        acc = add_t(acc, src[(int64_t)row * n + k]);
-      else
-        acc = add_t(acc, src[(int64_t)k * n + col]);
-    }
+    for (int k = 0; k < n; ++k) acc = add_t(acc, src[(int64_t)row * n + k]);
   }
   dest[(int64_t)row * n + col] = acc;
 }
