@@ -291,6 +291,7 @@ def model_report(wl, cal, app, mean_s: dict[str, float], dev=None) -> dict:
                 dt = time.perf_counter() - t0
                 g = dict(_errors(wl, app, m.predict_cpu(pr[0], app), ta), fit=sr[0],
                          seconds=round(dt, 4),
+                         params={n: float(v) for n, v in zip(m.params, pr[0])},
                          calibration_geomean_rel_error=_cal_err(m, pr[0], cal, tc))
                 if "reference_fit" in rep and "error" not in rep["reference_fit"]:
                     den = np.maximum(np.abs(p_ref), 1e-300)
@@ -321,6 +322,90 @@ def model_report(wl, cal, app, mean_s: dict[str, float], dev=None) -> dict:
                 params={n: float(v) for n, v in zip(m.params, params[best])})
         out[mname] = rep
     return out
+
+
+# ---------------------------------------------------------------------------
+# C5: the calibrated models evaluated over a large variant space (K18)
+
+
+def _concrete(vid: str, sizes: dict[str, int]) -> str:
+    gen, *parts = vid.split("__")
+    args = dict(p.split("-", 1) for p in parts)
+    args.update({k: str(v) for k, v in sizes.items()})
+    return "__".join([gen] + [f"{k}-{args[k]}" for k in sorted(args)])
+
+
+def c5_report(dev, parts, models: dict, heads: dict, npts: int = 1_000_000) -> dict:
+    """Every application variant of every workload, with its workload's
+    headline model and fitted parameters, evaluated at npts seeded points
+    (BASELINE.json configs[4]); winners per application. Checked against the
+    CPU port of the same tables and against the reference-API predict()."""
+    from paper_1904_09538_b200 import host, workloads
+    from paper_1904_09538_b200.predict import PredictionTables, c5_points
+    variants, coord_of = [], []
+    for g, (wl, _cal, app) in enumerate(parts):
+        h = heads[wl.name]
+        fit = models[wl.name].get(h["model"], {}).get(h["fit"] or "", {})
+        if "params" not in fit:
+            return {"error": f"{wl.name}: no fitted parameters"}
+        m = host.HostModel(wl.models[h["model"]])
+        params = [fit["params"][n] for n in m.params]
+        seen = set()
+        for vid in app:
+            key = workloads.variant_of(vid, wl.variant_keys)
+            if key in seen:
+                continue
+            seen.add(key)
+            variants.append({"id": vid, "model": wl.models[h["model"]], "params": params,
+                             "group": g, "coords": wl.c5_coords})
+            coord_of.append(wl.c5_coords)
+    t = PredictionTables(variants)
+    pts = c5_points(npts)
+    t.eval_gpu(dev, pts[:4096])  # warm
+    t0 = time.perf_counter()
+    pg, ag, ksec = t.eval_gpu(dev, pts)
+    wall = time.perf_counter() - t0
+    nsub = min(npts, 100_000)
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    pc, ac = t.eval_cpu(pts[:nsub], threads=threads)
+    cpu = time.perf_counter() - t0
+    rel = float(np.max(np.abs(pg[:nsub] - pc) / np.abs(pc)))
+    # ranking agreement, excluding exact near-ties (SURVEY A10)
+    mism = 0
+    for g in range(t.ngroups):
+        cols = [i for i, v in enumerate(variants) if v["group"] == g]
+        srt = np.sort(pc[:, cols], axis=1)
+        tie = (srt[:, 1] - srt[:, 0]) <= 1e-12 * np.abs(srt[:, 0])
+        mism += int(np.sum((ag[:nsub, g] != ac[:, g]) & ~tie))
+    # reference-API predict() (features through evaluate_feature) on a sample
+    nref = 64
+    t0 = time.perf_counter()
+    ref_rel = 0.0
+    for j in range(nref):
+        for v, var in enumerate(variants):
+            sizes = {k: int(pts[j, c]) for k, c in var["coords"].items()}
+            m = host.HostModel(var["model"])
+            r = m.predict_cpu(np.array(var["params"]), [_concrete(var["id"], sizes)])[0]
+            ref_rel = max(ref_rel, abs(pg[j, v] - r) / abs(r))
+    ref_t = time.perf_counter() - t0
+    winners = {}
+    for g, (wl, _c, _a) in enumerate(parts):
+        cols = [i for i, v in enumerate(variants) if v["group"] == g]
+        cnt = np.bincount(ag[:, g], minlength=t.nvar)  # argmin holds global variant indices
+        winners[wl.name] = {workloads.variant_of(variants[i]["id"], wl.variant_keys): int(cnt[i])
+                            for i in cols}
+    nev = npts * t.nvar
+    return {"points": npts, "variants": t.nvar, "evaluations": nev,
+            "gpu_kernel_ms": round(ksec * 1e3, 3),
+            "gpu_evals_per_s": round(nev / ksec, 1),
+            "gpu_e2e_ms": round(wall * 1e3, 2), "gpu_e2e_evals_per_s": round(nev / wall, 1),
+            "cpu_tables_evals_per_s": round(nsub * t.nvar / cpu, 1), "cpu_threads": threads,
+            "cpu_max_rel_diff": rel, "argmin_mismatches_vs_cpu": mism,
+            "reference_predict_evals_per_s": round(nref * t.nvar / ref_t, 1),
+            "reference_predict_max_rel_diff": ref_rel,
+            "reference_predict_sample": f"{nref} points x {t.nvar} variants through ps_predict_cpu",
+            "winners": winners}
 
 
 # ---------------------------------------------------------------------------
@@ -571,6 +656,11 @@ def run_ours(args, dist: Dist) -> None:
                           "geomean_rel_error": head.get("geomean_rel_error"),
                           "geomean_rel_error_all": head.get("geomean_rel_error_all"),
                           "ranking_correct": head.get("ranking_correct")}
+    try:
+        model_eval = (c5_report(dev, parts, models, heads, args.c5_points)
+                      if args.c5_points else None)
+    except Exception as e:  # reported, not hidden
+        model_eval = {"error": str(e)}
     n_app = sum(len(app) for _, _, app in parts)
     n_cal = len(kernels) - len({k for _, _, app in parts for k in app})
     line = {
@@ -596,6 +686,7 @@ def run_ours(args, dist: Dist) -> None:
         "ranking_correct": {w: h["ranking_correct"] for w, h in heads.items()},
         "headline": heads,
         "roofline": roofline,
+        "model_eval": model_eval,
         "roofline_hbm": roofline_hbm,
         "cpu_baseline": cpu_gmem_sample() if dist.world == 1 else None,
         "e2e": {"value": round(e2e_bytes_all / e2e_time_max / 1e9, 3) if e2e_time_max else None,
@@ -619,6 +710,8 @@ def main() -> None:
                     help="matmul | fd | dg | all (one sweep over the union, BASELINE configs[3])")
     ap.add_argument("--trials-per-step", type=int, default=4)
     ap.add_argument("--table", default="", help="write the measurement table (CSV) here")
+    ap.add_argument("--c5-points", type=int, default=1_000_000,
+                    help="parameter points for the model-evaluation report (0: skip)")
     ap.add_argument("--headline-model", default="",
                     help="model whose GPU fit is the headline (default: the workload's)")
     args = ap.parse_args()

@@ -74,7 +74,19 @@ __global__ void __launch_bounds__(128) eval_points_kernel(FlatTables t, const in
             for (int e = 0; e < t.term_exp[k * 4 + c]; ++e) term *= x[c];
           acc += term;
         }
-        f[j] = (double)(acc / t.feat_den[slot]);
+        const long long den = t.feat_den[slot];
+        if (den == 1) {
+          f[j] = (double)acc;
+        } else {  // Rational -> double as the host does: lowest terms, one division
+          __int128 a = acc < 0 ? -acc : acc, b = den;
+          while (b) {
+            const __int128 r = a % b;
+            a = b;
+            b = r;
+          }
+          f[j] = (a > 1) ? (double)(acc / a) / (double)(den / (long long)a)
+                         : (double)acc / (double)den;
+        }
       }
       const double y = eval_model_bc(t.ops + t.model_op_begin[m], t.model_op_begin[m + 1] - t.model_op_begin[m],
                                      t.consts + t.model_const_begin[m], t.params + t.model_param_begin[m], f);

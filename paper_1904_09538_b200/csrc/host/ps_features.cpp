@@ -256,13 +256,13 @@ Rational per_granularity(const Rational& raw, Granularity g, const KernelCounts&
     if (wg && wg % sgs != 0) {
       // Reference semantics: an error (features.cpp:318-326).
       // Opt-in extension: a work-group of wg work-items issues
-      // ceil(wg / sgs) sub-groups; counts that are per-work-item multiples of
-      // wg are converted at that rate, others must divide by sgs exactly.
+      // ceil(wg / sgs) sub-groups, so every sub-group entry converts at
+      // ceil(wg/sgs)/wg per work-item execution. The factor does not depend on
+      // the sizes (tabulable); the value need not be an integer.
       if (!g_round_up_subgroups.load())
         throw EvalError("work-group size " + std::to_string(wg) +
                         " is not a multiple of the sub-group size " + std::to_string(sgs));
-      Rational per_group = raw / Rational(wg);
-      if (is_integer(per_group)) return per_group * Rational((wg + sgs - 1) / sgs);
+      return raw * Rational((wg + sgs - 1) / sgs) / Rational(wg);
     }
   } else if (g == Granularity::work_group) {
     if (!c.geometry) throw EvalError("work-group granularity needs launch geometry");
@@ -273,6 +273,14 @@ Rational per_granularity(const Rational& raw, Granularity g, const KernelCounts&
     throw EvalError(what + ": count " + raw.str() + " is not divisible by the granularity divisor " +
                     std::to_string(div));
   return v;
+}
+
+// The symbolic counterpart of per_granularity for sub-group entries.
+Rational sub_group_factor(const KernelCounts& c, int sgs) {
+  const long long wg = c.geometry ? c.geometry->flat_work_group_size() : 0;
+  if (wg && wg % sgs != 0 && g_round_up_subgroups.load())
+    return Rational((wg + sgs - 1) / sgs) / Rational(wg);
+  return Rational(1, sgs);
 }
 
 }  // namespace
@@ -287,14 +295,16 @@ double evaluate_feature_counts(const FeatureSpec& spec, const KernelCounts& c,
       for (const auto& e : c.ops) {
         if (e.kind.dtype != spec.dtype || e.kind.op != spec.op) continue;
         val += per_granularity(e.count.eval(b), e.kind.gran, c, sgs, spec.id());
-        sym += e.count * Rational(1, sgs);
+        sym += e.count * sub_group_factor(c, sgs);
       }
       break;
     case FeatureSpec::Class::mem_access:
       for (const auto& e : c.accesses) {
         if (!pattern_matches(spec, e.pattern, b)) continue;
         val += per_granularity(e.count.eval(b), e.pattern.gran, c, sgs, spec.id());
-        sym += e.pattern.gran == Granularity::sub_group ? e.count * Rational(1, sgs) : e.count;
+        sym += e.pattern.gran == Granularity::sub_group
+                   ? e.count * sub_group_factor(c, sgs)
+                   : e.count;
       }
       break;
     case FeatureSpec::Class::sync:

@@ -107,6 +107,23 @@ VariantTables build_variant_tables(const std::string& spec_json) {
   return t;
 }
 
+// Rational::convert_to<double> of acc/den: reduce to lowest terms, then one
+// double division (ps_exact.hpp), so table values equal evaluate_feature's.
+double rational_to_double(__int128 acc, long long den) {
+  if (den == 1) return double(acc);
+  __int128 a = acc < 0 ? -acc : acc, b = den;
+  while (b) {
+    __int128 r = a % b;
+    a = b;
+    b = r;
+  }
+  if (a > 1) {
+    acc /= a;
+    den /= (long long)a;
+  }
+  return double(acc) / double(den);
+}
+
 std::vector<double> eval_point_cpu(const VariantTables& t, size_t v, const int64_t* point) {
   const size_t nf = size_t(t.model_nf[size_t(t.var_model[v])]);
   std::vector<double> f(nf);
@@ -119,7 +136,7 @@ std::vector<double> eval_point_cpu(const VariantTables& t, size_t v, const int64
         for (int e = 0; e < t.term_exp[size_t(k)][size_t(c)]; ++e) term *= point[c];
       acc += term;
     }
-    f[j] = double(acc / t.feat_den[slot]);
+    f[j] = rational_to_double(acc, t.feat_den[slot]);
   }
   return f;
 }

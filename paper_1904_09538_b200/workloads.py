@@ -130,6 +130,8 @@ class Workload:
     size_keys: tuple[str, ...] = ("n",)
     hbm_generators: tuple[str, ...] = ("gmem_pattern", "overlap_knl")
     extra: dict = field(default_factory=dict)
+    # C5 point column of each size parameter (predict.c5_points)
+    c5_coords: dict = field(default_factory=lambda: {"n": 0})
     # model whose GPU fit is the bench headline: the B200 LSU/FMA overlap model
     headline_model: str = "lsu"
 
@@ -172,6 +174,7 @@ FD = Workload(
     variant_keys=("tile",),
     size_keys=("n",),
     extra={"options": {"partial_subgroups": "round_up"}},
+    c5_coords={"n": 1},
 )
 
 DG_TAGS = ["dg-noPF-u", "dg-noPF-res", "dg-uPFnoPF-dm", "dg-uPF-u", "dg-uPF-res", "dg-dmPF-dm",
@@ -191,6 +194,7 @@ DG = Workload(
             "lsu": lsu_model(DG_GMEM, ONCHIP[:3], ONCHIP[3:])},
     variant_keys=("variant",),
     size_keys=("nelements",),
+    c5_coords={"nelements": 2, "nunit_nodes": 3},
 )
 
 WORKLOADS = {w.name: w for w in (MATMUL, FD, DG)}
