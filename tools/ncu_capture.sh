@@ -1,0 +1,23 @@
+#!/bin/bash
+# One `ncu --set full` capture per listed suite kernel (inputs resident,
+# 1 launch profiled), reports under gpurun_out/ncu_<tag>.ncu-rep, plus the
+# launch list of a short bench run. Run on the GPU box via gpurun.
+set -u
+out=gpurun_out
+mkdir -p $out
+cap() {  # tag kernel-regex variant-id
+  timeout 600 ncu --set full --clock-control none --import-source on -k "regex:$2" -s 1 -c 1 \
+    -o $out/ncu_$1 -f python tools/run_kernel.py "$3" 2 > $out/ncu_$1.log 2>&1
+  echo "$1 rc=$?"
+}
+cap mm_nopf_8192 matmul_nopf "matmul_sq__dtype-float32__groups_fit-True__lsize_0-16__lsize_1-16__n-8192__prefetch-False"
+cap mm_pf_4096 matmul_pf "matmul_sq__dtype-float32__groups_fit-True__lsize_0-16__lsize_1-16__n-4096__prefetch-True"
+cap fd16_8176 finite_diff_strip "finite_diff__dtype-float32__n-8176__tile-16x16"
+cap dg_upf_1e6 dg_upf "dg_diff__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-64__variant-uPF"
+cap dg_dmpft_1e6 dg_dmpf "dg_diff__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-64__variant-dmPFtrans"
+cap madd flops_pattern "flops_madd_pattern__dtype-float32__lid_stride_0-1__lid_stride_1-2048__lsize_0-16__lsize_1-16__m-128__nelements-2097152"
+cap gmem2 gmem_pattern "gmem_pattern__dtype-float32__lid_stride_0-1__lid_stride_1-2048__lsize_0-16__lsize_1-16__n_input_arrays-2__nelements-671088640"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+  --log-file $out/launches_all.csv python bench.py --steps 1 --warmup 1 --trials-per-step 1 \
+  --c5-points 100000 > $out/launches_bench.log 2>&1
+echo "launches rc=$?"
