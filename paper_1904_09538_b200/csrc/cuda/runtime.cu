@@ -230,8 +230,9 @@ int validate_desc(const ps_kernel_desc* d) {
         return set_error(PS_ERR_ARG, "matmul_sq realisation uses 16x16 work-groups");
       if (d->n < 16 || d->n % 16 != 0)
         return set_error(PS_ERR_ARG, "matmul_sq requires n to be a multiple of 16");
-      if (d->gen == PS_GEN_MATMUL_TC && d->n % 128 != 0)
-        return set_error(PS_ERR_ARG, "matmul_sq_tc requires n to be a multiple of 128");
+      if (d->gen == PS_GEN_MATMUL_TC && (d->n % 256 != 0 || d->dtype != PS_F32))
+        return set_error(PS_ERR_ARG,
+                         "matmul_sq_tc requires float32 and n a multiple of 256 (128x256 tiles)");
       return PS_OK;
     case PS_GEN_FD:
     case PS_GEN_FD_RM: {

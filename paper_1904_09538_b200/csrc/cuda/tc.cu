@@ -1,9 +1,278 @@
-// K16: tcgen05 dense-contraction matmul variant (placeholder until the
-// tcgen05/TMEM kernel lands; fails loudly instead of falling back).
+// K16: matmul_sq_tc — the extra dense-contraction variant on the 5th-gen
+// tensor cores (not a paper variant; BASELINE north_star "tensor cores appear
+// only in an extra tcgen05 matmul/DG variant flagged as a dense contraction").
+//
+// C[n][n] = A[n][n] . B[n][n], fp32 row-major in HBM, computed with
+// tcgen05.mma kind::tf32 (A and B read as TF32, FP32 accumulation in TMEM).
+// With the suite's seed-pattern inputs (small integers, tests/support.hpp:35-44)
+// every product and partial sum is exact, so the result equals the fp32
+// oracle bit for bit; on U[-1,1) inputs the TF32 operand rounding bounds the
+// error (stated in tests/test_gpu_parity.py).
+//
+// kind::tf32 takes K-major operands only (a transposed, N-major B is
+// silently ignored by the tensor core — measured on B200), so each launch
+// first writes Bt = B^T (n x n, coalesced 32x32 smem tiles, ~2 x 4n^2 bytes
+// of HBM traffic) and the GEMM reads A and Bt both K-major. The transpose is
+// part of the variant and inside the timed launch.
+//
+// One CTA per 128x256 output tile, 4 warps:
+//   warp 0 lane 0  TMA producer: per 32-wide K block, A 128x32 and Bt 256x32
+//                  (both K-major, one box each) into a 4-stage ring,
+//                  128-byte swizzle, mbarrier complete_tx;
+//   warp 1 lane 0  MMA issuer: 4 x tcgen05.mma (M=128, N=256, K=8) per stage,
+//                  tcgen05.commit frees the stage;
+//   warps 0-3      epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
+//                  32w..32w+31 = tile rows), 16-byte streaming stores.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "runtime_internal.h"
 
 namespace ps {
-int tc_launch(Ctx*, const ps_kernel_desc*) {
-  return set_error(PS_ERR_ARG, "matmul_sq_tc: tcgen05 variant not built in this revision");
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 32;  // BK: 32 fp32 = one 128-byte swizzle row
+constexpr int STAGES = 4;
+constexpr int UMMA_K = 8;                   // K per tcgen05.mma for kind::tf32
+constexpr int A_BYTES = BM * BK * 4;        // 16 KB
+constexpr int B_BYTES = BN * BK * 4;        // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr uint32_t TMEM_COLS = 256;         // 128 lanes x 256 fp32 columns
+
+// Instruction descriptor (cute/arch/mma_sm100_desc.hpp InstrDescriptor):
+// D f32, A/B tf32, both K-major, N>>3 at bit 17, M>>4 at bit 24.
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (0u << 16) |
+                           (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TC_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TC_WAIT;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+
+// Shared-memory matrix descriptor, 128-byte swizzle (cute UMMA::SmemDescriptor):
+// start >> 4 at [0,14), LBO >> 4 at [16,30), SBO >> 4 at [32,46), version 1 at
+// [46,48), layout SWIZZLE_128B (2) at [61,64).
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n}\n" ::"r"(
+          tmem_d),
+      "l"(da), "l"(db), "r"(IDESC), "r"(acc), "r"(0u)  // no output lanes disabled
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(128, 1)
+    matmul_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     float* __restrict__ C, int n) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sa = smem;                                    // STAGES x A tile (1024-aligned)
+  uint8_t* sb = smem + STAGES * A_BYTES;                 // STAGES x Bt tile
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + STAGES * B_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nk = n / BK;
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+  const uint32_t done = smem_u32(bars + 2 * STAGES);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {  // one warp allocates (and later frees) the accumulator columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // TMA producer
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(empty0 + 8 * s, ((kb / STAGES) - 1) & 1);
+      const uint32_t fb = full0 + 8 * s;
+      mbar_expect_tx(fb, STAGE_BYTES);
+      tma_load_2d(smem_u32(sa + s * A_BYTES), &tmA, fb, kb * BK, m0);
+      tma_load_2d(smem_u32(sb + s * B_BYTES), &tmB, fb, kb * BK, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // MMA issuer
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      mbar_wait(full0 + 8 * s, (kb / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t a_base = smem_u32(sa + s * A_BYTES), b_base = smem_u32(sb + s * B_BYTES);
+#pragma unroll
+      for (int ks = 0; ks < BK / UMMA_K; ++ks) {
+        // K-major, 128 B swizzle rows: advance 8 tf32 (32 B) inside the row;
+        // 8-row groups 1024 B apart (SBO); LBO unused (16 B)
+        const uint64_t da = desc_sw128(a_base + ks * UMMA_K * 4, 16, 1024);
+        const uint64_t db = desc_sw128(b_base + ks * UMMA_K * 4, 16, 1024);
+        mma_tf32(tmem, da, db, (kb | ks) != 0);
+      }
+      mma_commit(empty0 + 8 * s);  // stage s free once these MMAs have read it
+    }
+    mma_commit(done);
+  }
+
+  // epilogue: warp w reads TMEM lanes 32w..32w+31 (tile rows), 32 columns at a time
+  mbar_wait(done, 0);
+  __syncwarp();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int row = m0 + 32 * warp + lane;
+  float* crow = C + (int64_t)row * n + n0;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t v[32];
+    tmem_ld32(tmem + (uint32_t(32 * warp) << 16) + uint32_t(32 * c), v);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      __stcs(reinterpret_cast<float4*>(crow + 32 * c + 4 * q),
+             make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                         __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS)
+                 : "memory");
+}
+
+// Bt[j][i] = B[i][j], 32x32 tiles through shared memory (coalesced both ways).
+__global__ void __launch_bounds__(256) transpose_f32(const float* __restrict__ b,
+                                                     float* __restrict__ bt, int n) {
+  __shared__ float t[32][33];
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows per pass
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) t[r][tx] = __ldg(b + (int64_t)(y0 + r) * n + x0 + tx);
+  __syncthreads();
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) __stcs(bt + (int64_t)(x0 + r) * n + y0 + tx, t[tx][r]);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q{};
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D fp32 row-major [rows][cols] map with a box of box_cols x box_rows.
+int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, uint32_t box_cols,
+             uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return set_error(PS_ERR_CUDA, "matmul_sq_tc: cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(cols) * 4};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(PS_ERR_CUDA, "matmul_sq_tc: cuTensorMapEncodeTiled failed (%d)", int(r));
+  return PS_OK;
+}
+
+}  // namespace
+
+int tc_launch(Ctx* c, const ps_kernel_desc* d) {
+  if (d->dtype != PS_F32) return set_error(PS_ERR_ARG, "matmul_sq_tc is float32 (tf32 tensor cores)");
+  const int n = (int)d->n;
+  if (n % BN != 0) return set_error(PS_ERR_ARG, "matmul_sq_tc requires n to be a multiple of %d", BN);
+  static std::once_flag attr;
+  std::call_once(attr, [] {
+    cudaFuncSetAttribute(matmul_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  });
+  DevBuf& bt = c->scratch[7];
+  if (int rc = c->ensure(bt, size_t(n) * n * sizeof(float))) return rc;
+  CUtensorMap ta, tb;
+  int rc = make_map(&ta, c->in[0].ptr, n, n, BK, BM);  // A [m][k]: box 32 (k) x 128 (m)
+  if (rc) return rc;
+  rc = make_map(&tb, bt.ptr, n, n, BK, BN);            // Bt [n][k]: box 32 (k) x 256 (n)
+  if (rc) return rc;
+  transpose_f32<<<dim3(n / 32, n / 32), 256, 0, c->stream>>>((const float*)c->in[1].ptr,
+                                                             (float*)bt.ptr, n);
+  dim3 grid(n / BN, n / BM);
+  matmul_tc_kernel<<<grid, 128, SMEM_BYTES, c->stream>>>(ta, tb, (float*)c->out[0].ptr, n);
+  return PS_OK;
+}
+
 }  // namespace ps
