@@ -338,6 +338,56 @@ def model_report(wl, cal, app, mean_s: dict[str, float], dev=None) -> dict:
 
 
 # ---------------------------------------------------------------------------
+# K16: the extra tcgen05 dense-contraction variant (not a paper variant)
+
+
+def tensor_variant_report(dev, n: int = 8192, trials: int = 10) -> dict:
+    """matmul_sq_tc (tcgen05 kind::tf32, incl. its per-launch B transpose) at
+    n, timed like every suite kernel, next to cuBLAS TF32 (torch.matmul with
+    TF32 allowed) on the same shape, both with CUDA events."""
+    from paper_1904_09538_b200 import desc_from_id, kernel_io
+    vid = f"matmul_sq_tc__dtype-float32__lsize_0-16__lsize_1-16__n-{n}"
+    d = desc_from_id(vid)
+    io = kernel_io(d)
+    dev.prepare(d)
+    dev.measure(d, trials=3, warmup=0)
+    mean, kept = dev.measure_summary(d, trials=trials, warmup=2)
+    ours = io.flops / mean / 1e12
+    out = {"kernel": vid, "n": n, "tflops": round(ours, 1), "ms": round(mean * 1e3, 4),
+           "dtype": "tf32 operands, fp32 accumulate",
+           "note": "includes the per-launch B transpose (kind::tf32 needs K-major B)"}
+    pk, _src = peaks()
+    tf32_peak = pk.get("bf16_tflops", 1598.1) / 2
+    out["roofline"] = {"bound": "tensor", "achieved": round(ours, 1), "peak": round(tf32_peak, 1),
+                       "unit": "TFLOP/s", "frac": round(ours / tf32_peak, 4),
+                       "peak_source": "MEASURED_PEAKS.json bf16 dense / 2 (TF32 is half the "
+                                      "bf16 tensor rate; B200_PROFILING nominal 1.1 PF)"}
+    try:
+        import torch
+        torch.backends.cuda.matmul.allow_tf32 = True
+        a = torch.rand(n, n, device=f"cuda:{dev.device}", dtype=torch.float32)
+        b = torch.rand(n, n, device=f"cuda:{dev.device}", dtype=torch.float32)
+        for _ in range(3):
+            torch.matmul(a, b)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(trials):
+            torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        cub = e0.elapsed_time(e1) / 1e3 / trials
+        out["cublas_tf32_tflops"] = round(2.0 * n ** 3 / cub / 1e12, 1)
+        out["vs_cublas"] = round(ours / out["cublas_tf32_tflops"], 3)
+        del a, b
+        torch.cuda.empty_cache()
+    except Exception as e:  # reported, not hidden
+        out["cublas_tf32_tflops"] = None
+        out["cublas_error"] = str(e)
+    return out
+
+
+# ---------------------------------------------------------------------------
 # C5: the calibrated models evaluated over a large variant space (K18)
 
 
@@ -691,6 +741,10 @@ def run_ours(args, dist: Dist) -> None:
                       if args.c5_points else None)
     except Exception as e:  # reported, not hidden
         model_eval = {"error": str(e)}
+    try:
+        tensor_variant = tensor_variant_report(dev) if args.tc else None
+    except Exception as e:
+        tensor_variant = {"error": str(e)}
     n_app = sum(len(app) for _, _, app in parts)
     n_cal = len(kernels) - len({k for _, _, app in parts for k in app})
     line = {
@@ -719,6 +773,7 @@ def run_ours(args, dist: Dist) -> None:
         "headline": heads,
         "roofline": roofline,
         "model_eval": model_eval,
+        "tensor_variant": tensor_variant,
         "roofline_hbm": roofline_hbm,
         "cpu_baseline": cpu_gmem_sample() if dist.world == 1 else None,
         "e2e": {"value": round(e2e_bytes_all / e2e_time_max / 1e9, 3) if e2e_time_max else None,
@@ -742,6 +797,7 @@ def main() -> None:
                     help="matmul | fd | dg | all (one sweep over the union, BASELINE configs[3])")
     ap.add_argument("--trials-per-step", type=int, default=4)
     ap.add_argument("--table", default="", help="write the measurement table (CSV) here")
+    ap.add_argument("--tc", type=int, default=1, help="report the tcgen05 variant (0: skip)")
     ap.add_argument("--c5-points", type=int, default=1_000_000,
                     help="parameter points for the model-evaluation report (0: skip)")
     ap.add_argument("--headline-model", default="",
