@@ -4,8 +4,11 @@
 # launch list of a short bench run. Run on the GPU box via gpurun.
 set -u
 out=gpurun_out
+only=${1:-}
 mkdir -p $out
 cap() {  # tag kernel-regex variant-id
+  if [ -n "$only" ] && [ "$only" != "$1" ] && [ "$only" != "launches" ]; then return; fi
+  if [ "$only" = "launches" ]; then return; fi
   timeout 600 ncu --set full --clock-control none --import-source on -k "regex:$2" -s 1 -c 1 \
     -o $out/ncu_$1 -f python tools/run_kernel.py "$3" 2 > $out/ncu_$1.log 2>&1
   echo "$1 rc=$?"
@@ -16,8 +19,11 @@ cap fd16_8176 finite_diff_strip "finite_diff__dtype-float32__n-8176__tile-16x16"
 cap dg_upf_1e6 dg_upf "dg_diff__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-64__variant-uPF"
 cap dg_dmpft_1e6 dg_dmpf "dg_diff__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-64__variant-dmPFtrans"
 cap madd flops_pattern "flops_madd_pattern__dtype-float32__lid_stride_0-1__lid_stride_1-2048__lsize_0-16__lsize_1-16__m-128__nelements-2097152"
+cap tc_8192 matmul_tc_kernel "matmul_sq_tc__dtype-float32__lsize_0-16__lsize_1-16__n-8192"
 cap gmem2 gmem_pattern "gmem_pattern__dtype-float32__lid_stride_0-1__lid_stride_1-2048__lsize_0-16__lsize_1-16__n_input_arrays-2__nelements-671088640"
+if [ -z "$only" ] || [ "$only" = "launches" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
   --log-file $out/launches_all.csv python bench.py --steps 1 --warmup 1 --trials-per-step 1 \
-  --c5-points 100000 > $out/launches_bench.log 2>&1
+  --c5-points 100000 --tc 0 > $out/launches_bench.log 2>&1
 echo "launches rc=$?"
+fi
