@@ -15,14 +15,16 @@
 // of HBM traffic) and the GEMM reads A and Bt both K-major. The transpose is
 // part of the variant and inside the timed launch.
 //
-// One CTA per 128x256 output tile, 4 warps:
+// Persistent CTAs (one per SM) over 128x256 output tiles, 6 warps:
 //   warp 0 lane 0  TMA producer: per 32-wide K block, A 128x32 and Bt 256x32
 //                  (both K-major, one box each) into a 4-stage ring,
 //                  128-byte swizzle, mbarrier complete_tx;
-//   warp 1 lane 0  MMA issuer: 4 x tcgen05.mma (M=128, N=256, K=8) per stage,
-//                  tcgen05.commit frees the stage;
-//   warps 0-3      epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
-//                  32w..32w+31 = tile rows), 16-byte streaming stores.
+//   warp 1 lane 0  MMA issuer: 4 x tcgen05.mma (M=128, N=256, K=8) per stage
+//                  into one of two TMEM accumulators, tcgen05.commit frees
+//                  the stage / publishes the accumulator;
+//   warps 2-5      epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
+//                  32(w%4)..+31 = tile rows), 16-byte streaming stores,
+//                  overlapping the next tile's MMAs.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -117,7 +119,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(128, 1)
+// Persistent: one CTA per SM walks the output tiles (tile = blockIdx.x +
+// k * gridDim.x, 128-row blocks fastest inside bands of TILE_BAND column
+// blocks for L2 reuse). Two 256-column TMEM accumulators let the epilogue of
+// tile i drain while the MMAs of tile i+1 run. 6 warps: 0 TMA, 1 MMA,
+// 2-5 epilogue (warp w reads TMEM lanes 32*(w%4)..+31).
+constexpr int TILE_BAND = 8;
+
+__device__ __forceinline__ void tile_coords(int t, int mt, int& m0, int& n0) {
+  const int per_band = TILE_BAND * mt;
+  const int band = t / per_band, r = t - band * per_band;
+  m0 = (r % mt) * BM;
+  n0 = (band * TILE_BAND + r / mt) * BN;
+}
+
+__global__ void __launch_bounds__(192, 1)
     matmul_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      float* __restrict__ C, int n) {
   extern __shared__ uint8_t smem_raw[];
@@ -126,25 +142,28 @@ __global__ void __launch_bounds__(128, 1)
   uint8_t* sa = smem;                                    // STAGES x A tile (1024-aligned)
   uint8_t* sb = smem + STAGES * A_BYTES;                 // STAGES x Bt tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(sb + STAGES * B_BYTES);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nk = n / BK;
+  const int mt = n / BM, ntiles = mt * (n / BN);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
-  const uint32_t done = smem_u32(bars + 2 * STAGES);
+  const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
     }
-    mbar_init(done, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull0 + 8 * a, 1);
+      mbar_init(tempty0 + 8 * a, 128);  // every epilogue thread arrives
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) {  // one warp allocates (and later frees) the accumulator columns
+  if (warp == 0) {  // one warp allocates (and later frees) both accumulators
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS)
+                 "r"(2 * TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -153,57 +172,81 @@ __global__ void __launch_bounds__(128, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // TMA producer
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      if (kb >= STAGES) mbar_wait(empty0 + 8 * s, ((kb / STAGES) - 1) & 1);
-      const uint32_t fb = full0 + 8 * s;
-      mbar_expect_tx(fb, STAGE_BYTES);
-      tma_load_2d(smem_u32(sa + s * A_BYTES), &tmA, fb, kb * BK, m0);
-      tma_load_2d(smem_u32(sb + s * B_BYTES), &tmB, fb, kb * BK, n0);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // MMA issuer
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      mbar_wait(full0 + 8 * s, (kb / STAGES) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a_base = smem_u32(sa + s * A_BYTES), b_base = smem_u32(sb + s * B_BYTES);
-#pragma unroll
-      for (int ks = 0; ks < BK / UMMA_K; ++ks) {
-        // K-major, 128 B swizzle rows: advance 8 tf32 (32 B) inside the row;
-        // 8-row groups 1024 B apart (SBO); LBO unused (16 B)
-        const uint64_t da = desc_sw128(a_base + ks * UMMA_K * 4, 16, 1024);
-        const uint64_t db = desc_sw128(b_base + ks * UMMA_K * 4, 16, 1024);
-        mma_tf32(tmem, da, db, (kb | ks) != 0);
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer, stage ring continues across tiles
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int m0, n0;
+        tile_coords(t, mt, m0, n0);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(empty0 + 8 * s, ((it / STAGES) - 1) & 1);
+          const uint32_t fb = full0 + 8 * s;
+          mbar_expect_tx(fb, STAGE_BYTES);
+          tma_load_2d(smem_u32(sa + s * A_BYTES), &tmA, fb, kb * BK, m0);
+          tma_load_2d(smem_u32(sb + s * B_BYTES), &tmB, fb, kb * BK, n0);
+        }
       }
-      mma_commit(empty0 + 8 * s);  // stage s free once these MMAs have read it
     }
-    mma_commit(done);
-  }
-
-  // epilogue: warp w reads TMEM lanes 32w..32w+31 (tile rows), 32 columns at a time
-  mbar_wait(done, 0);
-  __syncwarp();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int row = m0 + 32 * warp + lane;
-  float* crow = C + (int64_t)row * n + n0;
-#pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
-    uint32_t v[32];
-    tmem_ld32(tmem + (uint32_t(32 * warp) << 16) + uint32_t(32 * c), v);
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int it = 0, local = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        const uint32_t d = tmem + uint32_t(acc * TMEM_COLS);
+        if (local >= 2) mbar_wait(tempty0 + 8 * acc, ((local >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(full0 + 8 * s, (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a_base = smem_u32(sa + s * A_BYTES), b_base = smem_u32(sb + s * B_BYTES);
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      __stcs(reinterpret_cast<float4*>(crow + 32 * c + 4 * q),
-             make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                         __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+          for (int ks = 0; ks < BK / UMMA_K; ++ks) {
+            // K-major, 128 B swizzle rows: advance 8 tf32 (32 B) inside the
+            // row; 8-row groups 1024 B apart (SBO); LBO unused (16 B)
+            const uint64_t da = desc_sw128(a_base + ks * UMMA_K * 4, 16, 1024);
+            const uint64_t db = desc_sw128(b_base + ks * UMMA_K * 4, 16, 1024);
+            mma_tf32(d, da, db, (kb | ks) != 0);
+          }
+          mma_commit(empty0 + 8 * s);  // stage s free once these MMAs have read it
+        }
+        mma_commit(tfull0 + 8 * acc);  // accumulator complete
+      }
+    }
+  } else {
+    // epilogue warps 2-5: TMEM lanes 32*(warp%4) .. +31 are tile rows
+    const int q4 = warp & 3;
+    int local = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+      int m0, n0;
+      tile_coords(t, mt, m0, n0);
+      const int acc = local & 1;
+      mbar_wait(tfull0 + 8 * acc, (local >> 1) & 1);
+      __syncwarp();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = m0 + 32 * q4 + lane;
+      float* crow = C + (int64_t)row * n + n0;
+      const uint32_t tbase = tmem + (uint32_t(32 * q4) << 16) + uint32_t(acc * TMEM_COLS);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tbase + uint32_t(32 * c), v);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          __stcs(reinterpret_cast<float4*>(crow + 32 * c + 4 * q),
+                 make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                             __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty0 + 8 * acc) : "memory");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS)
+                 "r"(2 * TMEM_COLS)
                  : "memory");
 }
 
@@ -270,8 +313,9 @@ int tc_launch(Ctx* c, const ps_kernel_desc* d) {
   if (rc) return rc;
   transpose_f32<<<dim3(n / 32, n / 32), 256, 0, c->stream>>>((const float*)c->in[1].ptr,
                                                              (float*)bt.ptr, n);
-  dim3 grid(n / BN, n / BM);
-  matmul_tc_kernel<<<grid, 128, SMEM_BYTES, c->stream>>>(ta, tb, (float*)c->out[0].ptr, n);
+  const int ntiles = (n / BM) * (n / BN);
+  const int grid = ntiles < c->sm_count ? ntiles : c->sm_count;
+  matmul_tc_kernel<<<grid, 192, SMEM_BYTES, c->stream>>>(ta, tb, (float*)c->out[0].ptr, n);
   return PS_OK;
 }
 
