@@ -20,6 +20,18 @@ __device__ __forceinline__ void sts_volatile(float* p, float v) {
   unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
   asm volatile("st.volatile.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
+// 32-byte read-only global load (sm_100 LDG.E.ENL2.256); p must be 32-byte aligned.
+struct f8 {
+  float v[8];
+};
+__device__ __forceinline__ f8 ldg256(const float* p) {
+  f8 r;
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+        "=f"(r.v[6]), "=f"(r.v[7])
+      : "l"(p));
+  return r;
+}
 __device__ __forceinline__ void bar_sync() { asm volatile("bar.sync 0;" ::: "memory"); }
 
 template <typename T>

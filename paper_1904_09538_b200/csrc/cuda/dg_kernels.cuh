@@ -31,26 +31,24 @@ __device__ __forceinline__ int64_t dg_res_idx(bool trans, const DgDims& d, int m
 }
 
 // noPF: no local memory; m outermost, reduction over j. The work-item's own
-// row reads along the sequential j are issued as 16-byte loads (Np is a
+// row reads along the sequential j are issued as 32-byte loads (Np is a
 // multiple of 16, so rows are 64-byte aligned): the same thread reads the same
-// elements and accumulates them in the same order, in a quarter of the load
+// elements and accumulates them in the same order, in an eighth of the load
 // instructions (each warp-wide u load touches 16 rows either way).
 __global__ void __launch_bounds__(256) dg_nopf(const float* __restrict__ dm,
                                                const float* __restrict__ u,
                                                float* __restrict__ res, DgDims d) {
   const int64_t k = (int64_t)blockIdx.x * 16 + threadIdx.x;
   const int i = blockIdx.y * 16 + threadIdx.y;
-  const float4* urow = reinterpret_cast<const float4*>(u + k * d.np);
+  const float* urow = u + k * d.np;
   for (int m = 0; m < d.nmat; ++m) {
-    const float4* dmrow = reinterpret_cast<const float4*>(dm + ((int64_t)m * d.np + i) * d.np);
+    const float* dmrow = dm + ((int64_t)m * d.np + i) * d.np;
     float acc = 0.f;
-#pragma unroll 4
-    for (int j4 = 0; j4 < d.np / 4; ++j4) {
-      const float4 a = __ldg(dmrow + j4), b = __ldg(urow + j4);
-      acc = __fmaf_rn(a.x, b.x, acc);
-      acc = __fmaf_rn(a.y, b.y, acc);
-      acc = __fmaf_rn(a.z, b.z, acc);
-      acc = __fmaf_rn(a.w, b.w, acc);
+#pragma unroll 2
+    for (int j8 = 0; j8 < d.np / 8; ++j8) {
+      const f8 a = ldg256(dmrow + 8 * j8), b = ldg256(urow + 8 * j8);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc = __fmaf_rn(a.v[q], b.v[q], acc);
     }
     res[dg_res_idx(false, d, m, k, i)] = acc;
   }
@@ -102,7 +100,8 @@ __global__ void __launch_bounds__(256) dg_upf(const float* __restrict__ dm,
 // memory (two barriers per tile); u read directly (strided by Np in dmPF,
 // unit-stride across lid(0) in the transposed layout). The work-item's
 // dm_fetch row is read 4 j_in at a time (LDS.128, pitch 20), and in dmPF its
-// u row too (LDG.128); FMAs in j_in order.
+// u row 8 at a time (32-byte loads); all 16 u loads of a j_out tile are issued
+// before its FMAs, which run in j_in order.
 template <bool TRANS>
 __global__ void __launch_bounds__(256) dg_dmpf(const float* __restrict__ dm,
                                                const float* __restrict__ u,
@@ -117,23 +116,32 @@ __global__ void __launch_bounds__(256) dg_dmpf(const float* __restrict__ dm,
       bar_sync();
       dmf[ly][lx] = dm[((int64_t)m * d.np + i0 + ly) * d.np + jo * 16 + lx];
       bar_sync();
+      if constexpr (TRANS) {
 #pragma unroll
-      for (int j4 = 0; j4 < 4; ++j4) {
-        const float4 a = *reinterpret_cast<const float4*>(&dmf[ly][4 * j4]);
-        float4 b;
-        if constexpr (TRANS) {
+        for (int j4 = 0; j4 < 4; ++j4) {
+          const float4 a = *reinterpret_cast<const float4*>(&dmf[ly][4 * j4]);
           const int j = jo * 16 + 4 * j4;
-          b.x = __ldg(u + (int64_t)j * d.nel + k);
-          b.y = __ldg(u + (int64_t)(j + 1) * d.nel + k);
-          b.z = __ldg(u + (int64_t)(j + 2) * d.nel + k);
-          b.w = __ldg(u + (int64_t)(j + 3) * d.nel + k);
-        } else {
-          b = __ldg(reinterpret_cast<const float4*>(u + k * d.np + jo * 16 + 4 * j4));
+          const float b0 = __ldg(u + (int64_t)j * d.nel + k);
+          const float b1 = __ldg(u + (int64_t)(j + 1) * d.nel + k);
+          const float b2 = __ldg(u + (int64_t)(j + 2) * d.nel + k);
+          const float b3 = __ldg(u + (int64_t)(j + 3) * d.nel + k);
+          acc = __fmaf_rn(a.x, b0, acc);
+          acc = __fmaf_rn(a.y, b1, acc);
+          acc = __fmaf_rn(a.z, b2, acc);
+          acc = __fmaf_rn(a.w, b3, acc);
         }
-        acc = __fmaf_rn(a.x, b.x, acc);
-        acc = __fmaf_rn(a.y, b.y, acc);
-        acc = __fmaf_rn(a.z, b.z, acc);
-        acc = __fmaf_rn(a.w, b.w, acc);
+      } else {
+        const f8 b0 = ldg256(u + k * d.np + jo * 16), b1 = ldg256(u + k * d.np + jo * 16 + 8);
+#pragma unroll
+        for (int j4 = 0; j4 < 4; ++j4) {
+          const float4 a = *reinterpret_cast<const float4*>(&dmf[ly][4 * j4]);
+          const f8& b = j4 < 2 ? b0 : b1;
+          const int o = 4 * (j4 & 1);
+          acc = __fmaf_rn(a.x, b.v[o], acc);
+          acc = __fmaf_rn(a.y, b.v[o + 1], acc);
+          acc = __fmaf_rn(a.z, b.v[o + 2], acc);
+          acc = __fmaf_rn(a.w, b.v[o + 3], acc);
+        }
       }
     }
     res[dg_res_idx(TRANS, d, m, k, i0 + ly)] = acc;
@@ -171,10 +179,13 @@ __global__ void __launch_bounds__(256) dg_rm(const float* __restrict__ src,
     if constexpr (VARIANT == 0) {
       // statement within (m, k, i), reduction j
       for (int m = 0; m < d.nmat; ++m) {
-        const float4* row = reinterpret_cast<const float4*>(
-            KEEP == 3 ? src + k * d.np : src + ((int64_t)m * d.np + i) * d.np);
-#pragma unroll 4
-        for (int j4 = 0; j4 < d.np / 4; ++j4) add4(__ldg(row + j4));
+        const float* row = KEEP == 3 ? src + k * d.np : src + ((int64_t)m * d.np + i) * d.np;
+#pragma unroll 2
+        for (int j8 = 0; j8 < d.np / 8; ++j8) {
+          const f8 v = ldg256(row + 8 * j8);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc = __fadd_rn(acc, v.v[q]);
+        }
       }
     } else if constexpr (VARIANT == 1) {
       if constexpr (KEEP == 3) {
@@ -207,15 +218,19 @@ __global__ void __launch_bounds__(256) dg_rm(const float* __restrict__ src,
     } else {
       if constexpr (KEEP == 3) {
         for (int m = 0; m < d.nmat; ++m)
-          for (int jo = 0; jo < njo; ++jo)
-            for (int j4 = 0; j4 < 4; ++j4) {
-              const int j = jo * 16 + 4 * j4;
-              if constexpr (TRANS) {
-                for (int q = 0; q < 4; ++q) acc = __fadd_rn(acc, src[dg_u_idx(true, d, k, j + q)]);
-              } else {
-                add4(__ldg(reinterpret_cast<const float4*>(src + k * d.np + j)));
-              }
+          for (int jo = 0; jo < njo; ++jo) {
+            if constexpr (TRANS) {
+              for (int j4 = 0; j4 < 4; ++j4)
+                for (int q = 0; q < 4; ++q)
+                  acc = __fadd_rn(acc, src[dg_u_idx(true, d, k, jo * 16 + 4 * j4 + q)]);
+            } else {
+              const f8 b0 = ldg256(src + k * d.np + jo * 16), b1 = ldg256(src + k * d.np + jo * 16 + 8);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) acc = __fadd_rn(acc, b0.v[q]);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) acc = __fadd_rn(acc, b1.v[q]);
             }
+          }
       } else {
         for (int m = 0; m < d.nmat; ++m)
           for (int jo = 0; jo < njo; ++jo)
