@@ -74,22 +74,25 @@ __global__ void __launch_bounds__(256) dg_upf(const float* __restrict__ dm,
     bar_sync();
     uf[ly][lx] = u[(k0 + ly) * d.np + jo * 16 + lx];  // u_fetch[k_in, j_in], j_in -> l.0
     bar_sync();
+    // the work-item's dm rows for this j_out: 2 x 32-byte loads per m, the
+    // same load shape as noPF's (dg-uPFnoPF-dm is one tag for both)
+    f8 dv[NMAT][2];
+#pragma unroll
+    for (int m = 0; m < NMAT; ++m) {
+      const float* row = dm + ((int64_t)m * d.np + i) * d.np + jo * 16;
+      dv[m][0] = ldg256(row);
+      dv[m][1] = ldg256(row + 8);
+    }
 #pragma unroll
     for (int j4 = 0; j4 < 4; ++j4) {
       const float4 uv = *reinterpret_cast<const float4*>(&uf[lx][4 * j4]);
-      float4 dv[NMAT];
+      const float u4[4] = {uv.x, uv.y, uv.z, uv.w};
 #pragma unroll
-      for (int m = 0; m < NMAT; ++m)
-        dv[m] = __ldg(reinterpret_cast<const float4*>(dm + ((int64_t)m * d.np + i) * d.np +
-                                                      jo * 16 + 4 * j4));
+      for (int q = 0; q < 4; ++q) {
+        const int j = 4 * j4 + q;
 #pragma unroll
-      for (int m = 0; m < NMAT; ++m) acc[m] = __fmaf_rn(dv[m].x, uv.x, acc[m]);
-#pragma unroll
-      for (int m = 0; m < NMAT; ++m) acc[m] = __fmaf_rn(dv[m].y, uv.y, acc[m]);
-#pragma unroll
-      for (int m = 0; m < NMAT; ++m) acc[m] = __fmaf_rn(dv[m].z, uv.z, acc[m]);
-#pragma unroll
-      for (int m = 0; m < NMAT; ++m) acc[m] = __fmaf_rn(dv[m].w, uv.w, acc[m]);
+        for (int m = 0; m < NMAT; ++m) acc[m] = __fmaf_rn(dv[m][j >> 3].v[j & 7], u4[q], acc[m]);
+      }
     }
   }
 #pragma unroll
@@ -192,27 +195,21 @@ __global__ void __launch_bounds__(256) dg_rm(const float* __restrict__ src,
         // fetch: one u load per (work-item, j_out)
         for (int jo = 0; jo < njo; ++jo) acc = __fadd_rn(acc, src[(k0 + ly) * d.np + jo * 16 + lx]);
       } else {
-        // the uPF update's dm reads: per j_out, 4 x nmat row quads in flight
+        // the uPF update's dm reads: per j_out, 2 x 32-byte loads per m
         for (int jo = 0; jo < njo; ++jo) {
-          float4 v[4][4];
+          f8 v[4][2];
 #pragma unroll
-          for (int j4 = 0; j4 < 4; ++j4)
+          for (int m = 0; m < 4; ++m)
+            if (m < d.nmat) {
+              const float* row = src + ((int64_t)m * d.np + i) * d.np + jo * 16;
+              v[m][0] = ldg256(row);
+              v[m][1] = ldg256(row + 8);
+            }
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
 #pragma unroll
             for (int m = 0; m < 4; ++m)
-              if (m < d.nmat)
-                v[j4][m] = __ldg(reinterpret_cast<const float4*>(
-                    src + ((int64_t)m * d.np + i) * d.np + jo * 16 + 4 * j4));
-#pragma unroll
-          for (int j4 = 0; j4 < 4; ++j4) {
-#pragma unroll
-            for (int m = 0; m < 4; ++m) if (m < d.nmat) acc = __fadd_rn(acc, v[j4][m].x);
-#pragma unroll
-            for (int m = 0; m < 4; ++m) if (m < d.nmat) acc = __fadd_rn(acc, v[j4][m].y);
-#pragma unroll
-            for (int m = 0; m < 4; ++m) if (m < d.nmat) acc = __fadd_rn(acc, v[j4][m].z);
-#pragma unroll
-            for (int m = 0; m < 4; ++m) if (m < d.nmat) acc = __fadd_rn(acc, v[j4][m].w);
-          }
+              if (m < d.nmat) acc = __fadd_rn(acc, v[m][j >> 3].v[j & 7]);
         }
       }
     } else {
