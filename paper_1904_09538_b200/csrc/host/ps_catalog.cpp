@@ -457,7 +457,7 @@ GeneratedKernel make_matmul_sq(const ArgMap& args) {
 }
 
 GeneratedKernel make_matmul_sq_rm(const ArgMap& args) {
-  const std::string& keep = str_arg(args, "keep");
+  const std::string keep = str_arg(args, "keep");
   const bool pf = bool_arg(args, "prefetch");
   ArgMap base_args = args;
   base_args.erase("keep");
@@ -470,7 +470,7 @@ GeneratedKernel make_matmul_sq_rm(const ArgMap& args) {
 
 GeneratedKernel make_fd_stencil(const ArgMap& args) {
   const Dtype dt = dtype_arg(args);
-  const std::string& tile = str_arg(args, "tile");
+  const std::string tile = str_arg(args, "tile");
   const long long n = int_arg(args, "n");
   long long T;
   if (tile == "16x16")
@@ -513,7 +513,7 @@ GeneratedKernel make_fd_stencil(const ArgMap& args) {
 }
 
 GeneratedKernel make_fd_stencil_rm(const ArgMap& args) {
-  const std::string& keep = str_arg(args, "keep");
+  const std::string keep = str_arg(args, "keep");
   ArgMap base_args = args;
   base_args.erase("keep");
   GeneratedKernel base = make_fd_stencil(base_args);
@@ -551,7 +551,7 @@ GeneratedKernel make_dg_diff(const ArgMap& args) {
   if (str_arg(args, "dtype") != "float32") throw SemanticError("dg_diff is float32");
   const Dtype dt = Dtype::float32;
   const bool trans = s.variant == "dmPFtrans";
-  const bool upf = s.variant == "uPF", dmpf = s.variant == "dmPF" || trans;
+  const bool upf = s.variant == "uPF";
   Builder b;
   b.param("nelements");
   b.param("nunit_nodes");
@@ -639,7 +639,7 @@ GeneratedKernel make_dg_diff(const ArgMap& args) {
 }
 
 GeneratedKernel make_dg_diff_rm(const ArgMap& args) {
-  const std::string& keep = str_arg(args, "keep");
+  const std::string keep = str_arg(args, "keep");
   ArgMap base_args = args;
   base_args.erase("keep");
   GeneratedKernel base = make_dg_diff(base_args);
