@@ -53,14 +53,19 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        # GPU of this rank; PS_BENCH_DEVICE pins every rank to one GPU (with
+        # PS_BENCH_BACKEND=gloo) to exercise the N>1 path on a 1-GPU box
+        self.device = int(os.environ.get("PS_BENCH_DEVICE", self.local_rank))
         self.pg = None
+        self.backend = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            backend = os.environ.get("PS_BENCH_BACKEND") or (
+                "nccl" if torch.cuda.is_available() else "gloo")
             if backend == "nccl":
-                torch.cuda.set_device(self.local_rank)
+                torch.cuda.set_device(self.device)
             dist.init_process_group(backend=backend)
             self.pg = dist
             self.backend = backend
@@ -69,7 +74,7 @@ class Dist:
         if self.pg:
             if self.backend == "nccl":
                 import torch
-                self.pg.barrier(device_ids=[self.local_rank])
+                self.pg.barrier(device_ids=[self.device])
                 torch.cuda.synchronize()
             else:
                 self.pg.barrier()
@@ -78,7 +83,7 @@ class Dist:
         if not self.pg:
             return x
         import torch
-        dev = f"cuda:{self.local_rank}" if self.backend == "nccl" else "cpu"
+        dev = f"cuda:{self.device}" if self.backend == "nccl" else "cpu"
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
@@ -89,7 +94,7 @@ class Dist:
         if not self.pg:
             return rows
         import torch
-        dev = f"cuda:{self.local_rank}" if self.backend == "nccl" else "cpu"
+        dev = f"cuda:{self.device}" if self.backend == "nccl" else "cpu"
         n = torch.tensor([len(rows)], dtype=torch.int64, device=dev)
         sizes = [torch.zeros_like(n) for _ in range(self.world)]
         self.pg.all_gather(sizes, n)
@@ -586,14 +591,14 @@ def run_ours(args, dist: Dist) -> None:
     mine = lpt(units, est, dist.world)[dist.rank]
     my_kernels = sorted({i for i, _ in mine})
 
-    dev = CudaDevice(dist.local_rank)
+    dev = CudaDevice(dist.device)
     for i in my_kernels:  # fill once; inputs stay resident in HBM
         dev.prepare(descs[i])
     for _ in range(args.warmup):
         for i, _t in mine:
             dev.measure(descs[i], trials=1, warmup=0)
 
-    sampler = ClockSampler(dist.local_rank)
+    sampler = ClockSampler(dist.device)
     sampler.start()
     time.sleep(0.5)
     dist.barrier()
@@ -644,7 +649,7 @@ def run_ours(args, dist: Dist) -> None:
     e2e_bytes_all = e2e_bytes
     if dist.pg:
         import torch
-        devn = f"cuda:{dist.local_rank}" if dist.backend == "nccl" else "cpu"
+        devn = f"cuda:{dist.device}" if dist.backend == "nccl" else "cpu"
         t = torch.tensor([e2e_bytes, float(h2d), float(d2h)], dtype=torch.float64, device=devn)
         dist.pg.all_reduce(t)
         e2e_bytes_all, h2d, d2h = t.tolist()
@@ -767,6 +772,8 @@ def run_ours(args, dist: Dist) -> None:
         # model and its GPU fit with the lowest CALIBRATION error
         "geomean_rel_error": {v: e for h in heads.values()
                               for v, e in (h["geomean_rel_error"] or {}).items()},
+        "geomean_rel_error_by_application": {w: h["geomean_rel_error_all"]
+                                             for w, h in heads.items()},
         "ranking_correct": {w: h["ranking_correct"] for w, h in heads.items()},
         "ranking_correct_gap_ge_2pct": {w: h["ranking_correct_gap_ge_2pct"]
                                         for w, h in heads.items()},
