@@ -4,7 +4,10 @@
 #define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
 #include "doctest.h"
 
+#include <cstdlib>
+
 #include "perfseer/counting.hpp"
+#include "perfseer/manifest.hpp"
 #include "perfseer/oracle.hpp"
 #include "perfseer/uipick.hpp"
 
@@ -109,4 +112,22 @@ TEST_CASE("every B200 catalog variant id round-trips through kernel_from_variant
     CHECK(again.kernel == g.kernel);
     CHECK(again.bindings == g.bindings);
   }
+}
+
+TEST_CASE("run manifest: reproducible with SOURCE_DATE_EPOCH (manifest.cpp:10-49)") {
+  setenv("SOURCE_DATE_EPOCH", "1700000000", 1);
+  const RunManifest m = make_manifest("perfseer calibrate --model m.txt", {{"model", file_hash_hex("")},
+                                                                          {"table", file_hash_hex("a")}},
+                                      7);
+  unsetenv("SOURCE_DATE_EPOCH");
+  // the reference's FNV-1a offset basis is 1469598103934665603 (one digit
+  // short of the standard 14695981039346656037, kernel_json.cpp:246), so
+  // "" -> 14650fb0739d0383 and "a" -> 44bd8ad473cd9906
+  CHECK(m.input_hashes.at("model") == "14650fb0739d0383");
+  CHECK(m.input_hashes.at("table") == "44bd8ad473cd9906");
+  CHECK(m.to_json().dump() ==
+        "{\"command\":\"perfseer calibrate --model m.txt\",\"input_hashes\":{\"model\":"
+        "\"14650fb0739d0383\",\"table\":\"44bd8ad473cd9906\"},\"seed\":7,\"timestamp\":"
+        "\"1700000000\",\"tool_version\":\"0.1.0\"}");
+  CHECK(m.comment_line().rfind("# manifest: {", 0) == 0);
 }
