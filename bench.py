@@ -343,6 +343,48 @@ def model_report(wl, cal, app, mean_s: dict[str, float], dev=None) -> dict:
 
 
 # ---------------------------------------------------------------------------
+# Overlap diagnosis (executor.cpp:169-174)
+
+
+def overlap_diagnosis(parts, models: dict, mean_s: dict[str, float]) -> dict:
+    """classify_overlap on real work-removed timings: per application variant
+    (at every size that has work-removed kernels), full time vs the sum of its
+    `_rm` kernels plus the on-chip estimate of the calibrated linear model;
+    'max_overlap' when that sum exceeds the full time by > 15%."""
+    from paper_1904_09538_b200 import host, workloads
+    onchip = [("p_f32add", workloads.OPS["add"]), ("p_f32mul", workloads.OPS["mul"]),
+              ("p_f32madd", workloads.OPS["madd"]), ("p_f32l", workloads.LMEM)]
+
+    def split(v):
+        g, *p = v.split("__")
+        return g, dict(x.split("-", 1) for x in p)
+
+    out = {}
+    for wl, _cal, app in parts:
+        fit = models.get(wl.name, {}).get("linear", {}).get("gpu_reference_fit", {})
+        if "params" not in fit:
+            continue
+        lin = host.HostModel(wl.models["linear"])
+        feats = dict(zip(app, lin.feature_table(app)))
+        per = {}
+        for vid in app:
+            g, a = split(vid)
+            rm = [k for k in mean_s if k.startswith(g + "_rm__")
+                  and all(split(k)[1].get(x) == y for x, y in a.items())]
+            if not rm:
+                continue
+            f = dict(zip(lin.features, feats[vid]))
+            est = sum(fit["params"][pn] * f.get(fn, 0.0) for pn, fn in onchip)
+            full, removed = mean_s[vid], sum(mean_s[k] for k in rm)
+            kind = "max_overlap" if removed + est > full * 1.15 else "linear"
+            key = workloads.variant_of(vid, wl.variant_keys)
+            per.setdefault(key, {})[workloads.size_of(vid, wl.size_keys)] = {
+                "full_s": full, "removed_s": removed, "onchip_s": est, "kind": kind}
+        out[wl.name] = per
+    return out
+
+
+# ---------------------------------------------------------------------------
 # K16: the extra tcgen05 dense-contraction variant (not a paper variant)
 
 
@@ -747,6 +789,10 @@ def run_ours(args, dist: Dist) -> None:
     except Exception as e:  # reported, not hidden
         model_eval = {"error": str(e)}
     try:
+        diagnosis = overlap_diagnosis(parts, models, mean_s)
+    except Exception as e:
+        diagnosis = {"error": str(e)}
+    try:
         tensor_variant = tensor_variant_report(dev) if args.tc else None
     except Exception as e:
         tensor_variant = {"error": str(e)}
@@ -781,6 +827,7 @@ def run_ours(args, dist: Dist) -> None:
         "roofline": roofline,
         "model_eval": model_eval,
         "tensor_variant": tensor_variant,
+        "overlap_diagnosis": diagnosis,
         "roofline_hbm": roofline_hbm,
         "cpu_baseline": cpu_gmem_sample() if dist.world == 1 else None,
         "e2e": {"value": round(e2e_bytes_all / e2e_time_max / 1e9, 3) if e2e_time_max else None,
