@@ -268,6 +268,13 @@ int ps_model_bytecode(const char* model_text, int which, int32_t* ops, int cap_o
 /* Process-wide options of the host port. "partial_subgroups" = "strict"
  * (reference: sub-group counts need wg % 32 == 0, features.cpp:318-326) or
  * "round_up" (a work-group issues ceil(wg/32) sub-groups). */
+/* Exact counts of a generated variant at its own bindings (SPEC acceptance 1
+ * at any size), as JSON {"ops", "access_counts", "access_footprints",
+ * "footprints", "barrier_local", "group_launch"}: mode 0 = symbolic
+ * (counting.cpp analyze), 1 = CPU enumeration (oracle.cpp:429-443
+ * brute_force_count), 2 = the same enumeration on the GPU of ctx. */
+int ps_enumerate(ps_ctx* ctx, const char* variant_id, int mode, char* out, size_t cap,
+                 size_t* needed);
 int ps_set_option(const char* key, const char* value);
 /* geo_mean_rel_error (executor.cpp:50-61). */
 int ps_geo_mean_rel_error(const double* pred, const double* meas, int n, double* out);

@@ -58,6 +58,55 @@ NumericPattern evaluate_pattern(const AccessPattern& p, const std::map<std::stri
   return n;
 }
 
+NumericPattern probe_pattern(const Kernel& k, const Statement& s, const Access& a, Direction dir,
+                             const std::vector<std::string>& binders,
+                             const std::map<std::string, long long>& b) {
+  std::map<int, std::string> local, group;
+  for (const auto& [iname, tag] : k.iname_tags) {
+    if (tag.kind == InameTag::Kind::local) local[tag.axis] = iname;
+    if (tag.kind == InameTag::Kind::group) group[tag.axis] = iname;
+  }
+  const ArgDecl& decl = k.arg(a.array);
+  NumericPattern p;
+  p.mem = decl.space == MemSpace::local ? "local" : "global";
+  p.dir = direction_str(dir);
+  p.dtype_bytes = dtype_bytes(decl.dtype);
+  p.tag = a.tag;
+  std::vector<long long> row(decl.shape.size(), 1);
+  for (size_t d = decl.shape.size(); d-- > 1;) row[d - 1] = row[d] * eval_int(decl.shape[d], b);
+  auto flat = [&](const Env& env) {
+    long long f = 0;
+    for (size_t d = 0; d < a.subs.size(); ++d) f += eval_int(a.subs[d], env) * row[d];
+    return f;
+  };
+  // d(flat)/d(iname) measured at two base points; affine => equal.
+  auto slope = [&](const std::string& iname) {
+    long long d[2];
+    for (int base = 0; base < 2; ++base) {
+      Env e = b;
+      for (const auto& o : k.domain.inames) e[o] = base;
+      const long long f0 = flat(e);
+      e[iname] += 1;
+      d[base] = flat(e) - f0;
+    }
+    if (d[0] != d[1]) throw EvalError("non-affine subscript on '" + a.array + "'");
+    return d[0];
+  };
+  for (const auto& [axis, i] : local) p.lstrides[axis] = slope(i);
+  for (const auto& [axis, i] : group) p.gstrides[axis] = slope(i);
+  std::vector<std::string> order = k.ordered_within(s);
+  order.insert(order.end(), binders.begin(), binders.end());
+  for (auto it = order.rbegin(); it != order.rend(); ++it)
+    if (k.is_sequential(*it)) {
+      p.has_loop_stride = true;
+      p.loop_stride = slope(*it);
+      break;
+    }
+  const bool uniform = p.lstrides.count(0) && p.lstrides.at(0) == 0;
+  p.gran = (p.mem == "local" || uniform) ? "sub_group" : "work_item";
+  return p;
+}
+
 namespace {
 
 class Visitor {
@@ -155,45 +204,7 @@ class Visitor {
 
   NumericPattern probe(const Statement& s, const Access& a, Direction dir,
                        const std::vector<std::string>& binders) {
-    const ArgDecl& decl = k_.arg(a.array);
-    NumericPattern p;
-    p.mem = decl.space == MemSpace::local ? "local" : "global";
-    p.dir = direction_str(dir);
-    p.dtype_bytes = dtype_bytes(decl.dtype);
-    p.tag = a.tag;
-    std::vector<long long> row(decl.shape.size(), 1);
-    for (size_t d = decl.shape.size(); d-- > 1;) row[d - 1] = row[d] * eval_int(decl.shape[d], b_);
-    auto flat = [&](const Env& env) {
-      long long f = 0;
-      for (size_t d = 0; d < a.subs.size(); ++d) f += eval_int(a.subs[d], env) * row[d];
-      return f;
-    };
-    // d(flat)/d(iname) measured at two base points; affine => equal.
-    auto slope = [&](const std::string& iname) {
-      long long d[2];
-      for (int base = 0; base < 2; ++base) {
-        Env e = b_;
-        for (const auto& o : k_.domain.inames) e[o] = base;
-        const long long f0 = flat(e);
-        e[iname] += 1;
-        d[base] = flat(e) - f0;
-      }
-      if (d[0] != d[1]) throw EvalError("non-affine subscript on '" + a.array + "'");
-      return d[0];
-    };
-    for (const auto& [axis, i] : local_) p.lstrides[axis] = slope(i);
-    for (const auto& [axis, i] : group_) p.gstrides[axis] = slope(i);
-    std::vector<std::string> order = k_.ordered_within(s);
-    order.insert(order.end(), binders.begin(), binders.end());
-    for (auto it = order.rbegin(); it != order.rend(); ++it)
-      if (k_.is_sequential(*it)) {
-        p.has_loop_stride = true;
-        p.loop_stride = slope(*it);
-        break;
-      }
-    const bool uniform = p.lstrides.count(0) && p.lstrides.at(0) == 0;
-    p.gran = (p.mem == "local" || uniform) ? "sub_group" : "work_item";
-    return p;
+    return probe_pattern(k_, s, a, dir, binders, b_);
   }
 
   void add_site(const Statement& s, const Access& a, Direction dir, const std::vector<std::string>& binders) {

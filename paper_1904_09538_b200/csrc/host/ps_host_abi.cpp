@@ -9,6 +9,7 @@
 #include "../cuda/runtime_internal.h"
 #include "json.hpp"
 #include "ps_catalog.hpp"
+#include "ps_enumerate.hpp"
 #include "ps_executor.hpp"
 #include "ps_model.hpp"
 
@@ -341,3 +342,51 @@ int ps_eval_cpu(const ps_tables* tables, const int64_t* points, int64_t npts, do
 }
 
 }  // extern "C"
+
+// SPEC acceptance 1 at any size: symbolic counts (analyze), the CPU
+// enumerator (brute_force_count, oracle.cpp:429-443) or the GPU enumerator,
+// as one JSON record of the variant at its own bindings.
+int ps_enumerate(ps_ctx* ctx, const char* variant_id, int mode, char* out, size_t cap,
+                 size_t* needed) {
+  return guarded([&] {
+    const GeneratedKernel g = kernel_from_variant_id(variant_id ? variant_id : "");
+    nlohmann::json j;
+    auto ll = [&](const Poly& p) {
+      const Rational v = p.eval(g.bindings);
+      if (!is_integer(v)) throw EvalError("non-integral count");
+      return numerator(v).convert_to<long long>();
+    };
+    if (mode == 0) {
+      const KernelCounts c = analyze(g.kernel);
+      std::map<std::string, long long> ops, acc, fp;
+      for (const auto& e : c.ops)
+        if (long long v = ll(e.count)) ops[e.kind.key()] += v;
+      for (const auto& e : c.accesses)
+        if (long long v = ll(e.count)) acc[evaluate_pattern(e.pattern, g.bindings).key()] += v;
+      for (const auto& [a, p] : c.footprints) fp[a] = ll(p);
+      long long bar = 0;
+      for (const auto& e : c.sync)
+        if (e.kind == SyncKind::barrier_local) bar = ll(e.count);
+      j["ops"] = ops;
+      j["access_counts"] = acc;
+      j["footprints"] = fp;
+      j["barrier_local"] = bar;
+    } else {
+      if (mode == 2 && !ctx) throw EvalError("ps_enumerate: GPU mode needs a context");
+      const OracleCounts o = mode == 2 ? brute_force_count_gpu(ctx, g.kernel, g.bindings)
+                                       : brute_force_count(g.kernel, g.bindings, 2'000'000'000LL);
+      std::map<std::string, long long> ops, acc;
+      for (const auto& [k, v] : o.ops)
+        if (v) ops[k] = v;
+      for (const auto& [k, v] : o.access_counts)
+        if (v) acc[k] = v;
+      j["ops"] = ops;
+      j["access_counts"] = acc;
+      j["access_footprints"] = o.access_footprints;
+      j["footprints"] = o.footprints;
+      j["barrier_local"] = o.barrier_local;
+      j["group_launch"] = o.group_launch;
+    }
+    return copy_out(j.dump(), out, cap, needed);
+  });
+}

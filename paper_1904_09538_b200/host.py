@@ -131,6 +131,18 @@ class HostModel:
             return ops[: n_ops.value].copy(), consts[: n_consts.value].copy(), stack.value
 
 
+def enumerate_counts(variant_id: str, mode: str = "symbolic", dev=None) -> dict:
+    """Exact counts of a variant at its own bindings: mode "symbolic"
+    (analyze), "cpu" (brute_force_count) or "gpu" (the enumerator on dev)."""
+    L = _declare()
+    L.ps_enumerate.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_char_p, C.c_size_t,
+                               _P(C.c_size_t)]
+    L.ps_enumerate.restype = C.c_int
+    m = {"symbolic": 0, "cpu": 1, "gpu": 2}[mode]
+    ctx = dev._ctx if dev is not None else None
+    return json.loads(_string_call(L.ps_enumerate, ctx, variant_id.encode(), m))
+
+
 def set_option(key: str, value: str) -> None:
     """ps_set_option, e.g. ("partial_subgroups", "round_up") for 18x18 tiles."""
     L = _declare()
