@@ -780,16 +780,19 @@ std::vector<Generator> b200_generators() {
   out.push_back(gen("finite_diff_rm",
                     {{"dtype", {"float32"}}, {"tile", {"16x16", "18x18"}}, {"keep", {"u", "res"}}, {"n", fd_n}},
                     make_fd_stencil_rm));
-  // BASELINE.json config 2: DG, 10^4..10^6 elements, nunit_nodes 64 (the
-  // paper's setting) plus padded orders for prediction sweeps.
-  const std::vector<std::string> dg_nel{"10000", "100000", "400000", "1000000"};
+  // BASELINE.json config 2: DG, 3-D orders 1-7, 10^4..10^6 elements. Nodes
+  // per element (k+1)(k+2)(k+3)/6 = 4, 10, 20, 35, 56, 84, 120 padded to the
+  // 16-wide work-group: 16 (orders 1 and 2), 32, 48, 64, 96, 128;
+  // Np = 64 is also the paper's own setting.
+  const std::vector<std::string> dg_np{"16", "32", "48", "64", "96", "128"};
   out.push_back(gen("dg_diff",
                     {{"dtype", {"float32"}}, {"variant", {"noPF", "uPF", "dmPF", "dmPFtrans"}},
-                     {"nmatrices", {"3"}}, {"nunit_nodes", {"64"}}, {"nelements", dg_nel}},
+                     {"nmatrices", {"3"}}, {"nunit_nodes", dg_np},
+                     {"nelements", {"10000", "100000", "1000000"}}},
                     make_dg_diff));
   out.push_back(gen("dg_diff_rm",
                     {{"dtype", {"float32"}}, {"variant", {"noPF", "uPF", "dmPF", "dmPFtrans"}},
-                     {"keep", {"u", "dm", "res"}}, {"nmatrices", {"3"}}, {"nunit_nodes", {"64"}},
+                     {"keep", {"u", "dm", "res"}}, {"nmatrices", {"3"}}, {"nunit_nodes", dg_np},
                      {"nelements", {"100000", "1000000"}}},
                     make_dg_diff_rm));
   return out;

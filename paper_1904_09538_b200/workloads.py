@@ -184,7 +184,8 @@ DG_GMEM = [("p_g16", G16)] + [("p_" + t.replace("-", "_"), _tag(t)) for t in DG_
 DG = Workload(
     name="dg",
     description=("BASELINE.json configs[2]: DG differentiation res[m,k,i] = sum_j dm[m,i,j] u[k,j], "
-                 "4 variants (noPF, uPF, dmPF, dmPFtrans), nmat=3, Np=64, nel 10^4..10^6, "
+                 "4 variants (noPF, uPF, dmPF, dmPFtrans), nmat=3, 3-D orders 1-7 (Np padded to "
+                 "16, 32, 48, 64, 96, 128), nel 10^4..10^6, "
                  "calibrated from the microbenchmark sweep plus the 10 dg-* work-removed tags "
                  "(PAPER.md:2041-2050, 2354-2505)"),
     calibration_tags=MICRO_TAGS + [["dg_diff_rm"]],
@@ -193,7 +194,7 @@ DG = Workload(
             "max3": max3_model(DG_GMEM, ONCHIP[:3], ONCHIP[3:]),
             "lsu": lsu_model(DG_GMEM, ONCHIP[:3], ONCHIP[3:])},
     variant_keys=("variant",),
-    size_keys=("nelements",),
+    size_keys=("nelements", "nunit_nodes"),
     c5_coords={"nelements": 2, "nunit_nodes": 3},
 )
 

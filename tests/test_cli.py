@@ -1,0 +1,174 @@
+"""The `perfseer` command line (paper_1904_09538_b200/bin/perfseer, reference
+tools/perfseer.cpp:475-583; SPEC.md MODULE cli examples): the paper's
+five-step workflow on the synthetic device end to end, reference filter
+counts, exit codes and byte-reproducible reruns; the B200 executor behind
+`measure --device cuda:0` on the GPU."""
+from __future__ import annotations
+
+import csv
+import json
+import os
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+CLI = ROOT / "paper_1904_09538_b200" / "bin" / "perfseer"
+
+TAGS = ["matmul_sq", "dtype:float32", "lsize_0:16", "lsize_1:16", "groups_fit:True",
+        "n:2048,2560,3072,3584"]
+DEVICE = {
+    "schema": "perfseer-device/1", "name": "dev", "combine": "linear",
+    "overhead_kernel": 5e-6, "overhead_group": 0.0,
+    "cost_table": [
+        {"feature": "f_op_float32_madd", "bucket": "onchip", "seconds_per_unit": 2e-13},
+        {"feature": "f_mem_access_global_float32", "bucket": "gmem", "seconds_per_unit": 3e-12},
+    ],
+}
+MODEL = ("f_exec_wall_time_synthetic_dev\n"
+         "p_madd * f_op_float32_madd + p_g * f_mem_access_global_float32"
+         " + p_launch * f_sync_kernel_launch\n")
+
+
+def run(*args, cwd, check=True, env=None):
+    r = subprocess.run([str(CLI), *map(str, args)], cwd=cwd, capture_output=True, text=True,
+                       env=env, timeout=120)
+    if check and r.returncode != 0:
+        raise AssertionError(f"perfseer {' '.join(map(str, args))}: rc {r.returncode}\n{r.stderr}")
+    return r
+
+
+@pytest.fixture(scope="module")
+def cli():
+    if not CLI.exists():
+        subprocess.run(["make", "-C", str(ROOT / "paper_1904_09538_b200" / "csrc"), "-j8"], check=True)
+    return CLI
+
+
+def pipeline(d: Path, extra_env=None) -> None:
+    env = dict(os.environ, **(extra_env or {}))
+    (d / "dev.json").write_text(json.dumps(DEVICE))
+    (d / "m.txt").write_text(MODEL)
+    run("generate", *[a for t in TAGS for a in ("--tag", t)], "--out", "k", cwd=d, env=env)
+    run("--seed", 7, "measure", "--device", "dev.json", "--kernels", "k", "--trials", 5,
+        "--out", "meas.csv", cwd=d, env=env)
+    run("features", "--model", "m.txt", "--kernels", "k", "--out", "f.csv", cwd=d, env=env)
+    run("calibrate", "--model", "m.txt", "--features", "f.csv", "--measurements", "meas.csv",
+        "--out", "cal.json", cwd=d, env=env)
+    run("predict", "--model", "cal.json", "--kernels", "k", "--out", "pred.csv", cwd=d, env=env)
+    run("report", "--measured", "meas.csv", "--predicted", "pred.csv", "--manifest",
+        "k/manifest.json", "--out", "rep", cwd=d, env=env)
+
+
+def test_version_and_usage(cli, tmp_path):
+    assert run("--version", cwd=tmp_path).stdout.strip() == "perfseer 0.1.0"
+    r = run("frobnicate", cwd=tmp_path, check=False)
+    assert r.returncode == 1 and r.stderr.startswith("error: unknown command")
+
+
+def test_generate_matches_reference_filter(cli, tmp_path):
+    # SPEC acceptance 5: the 2.2 tag set gives 4 kernels, 8 without prefetch:True
+    run("generate", *[a for t in TAGS + ["prefetch:True"] for a in ("--tag", t)], "--out", "a",
+        cwd=tmp_path)
+    man = json.loads((tmp_path / "a" / "manifest.json").read_text())
+    assert len(man["kernels"]) == 4
+    (tmp_path / "tags.txt").write_text("# 2.2\n" + "\n".join(TAGS) + "\n")
+    run("generate", "--tags", "tags.txt", "--out", "b", cwd=tmp_path)
+    man = json.loads((tmp_path / "b" / "manifest.json").read_text())
+    assert len(man["kernels"]) == 8 and "tags" in man["manifest"]["input_hashes"]
+    from paper_1904_09538_b200 import host
+    assert [k["id"] for k in man["kernels"]] == [k for k, _ in host.catalog(TAGS, which="reference")]
+    r = run("generate", "--tag", "matmul_sq", "--tag", "finite_diff", "--out", "c", cwd=tmp_path)
+    assert "no generators matched" in r.stderr
+    run("generate", "--tag", "matmul_sq", "--tag", "finite_diff", "--match", "intersect",
+        "--out", "d", cwd=tmp_path)
+    gens = {k["generator"] for k in json.loads((tmp_path / "d" / "manifest.json").read_text())["kernels"]}
+    assert gens == {"matmul_sq", "finite_diff"}
+
+
+def test_count_known_answers(cli, tmp_path):
+    # test_counting.cpp:88-101: madd n^3; noPF a uniform (per sub-group), b loop stride n
+    run("generate", *[a for t in TAGS + ["prefetch:False", "n:2048"] for a in ("--tag", t)],
+        "--out", "k", cwd=tmp_path)
+    kf = next(p for p in (tmp_path / "k").iterdir() if p.name.startswith("matmul_sq"))
+    j = json.loads(run("count", "--kernel", kf, "--bind", "n=64", cwd=tmp_path).stdout)
+    madd = [o for o in j["ops"] if o["op"] == "madd"]
+    assert madd[0]["count"] == "n^3" and madd[0]["value"] == {"num": str(64 ** 3), "den": "1"}
+    pats = {a["pattern"].split(":")[4]: a for a in j["accesses"]}
+    assert pats["tag=mm-noPF-a"]["granularity"] == "sub_group"
+    assert pats["tag=mm-noPF-b"]["pattern"].endswith("loop=n")
+    assert j["footprints"]["a"]["count"] == "n^2"
+    assert j["geometry"]["work_group_size"] == [16, 16]
+    # without a binding the symbolic counts remain, values are null
+    j = json.loads(run("count", "--kernel", kf, cwd=tmp_path).stdout)
+    assert j["ops"][0]["value"] is None and j["manifest"]["command"] == "count"
+
+
+def test_five_step_workflow_synthetic(cli, tmp_path):
+    pipeline(tmp_path)
+    cal = json.loads((tmp_path / "cal.json").read_text())
+    assert cal["schema"] == "perfseer-calibrated-model/1" and cal["converged"]
+    # sigma = 0: the hidden cost table is recovered (SPEC acceptance 6 tolerance 0.1%)
+    want = {"p_madd": 2e-13, "p_g": 3e-12, "p_launch": 5e-6}
+    for k, v in want.items():
+        assert abs(cal["param_values"][k] - v) <= 1e-3 * v
+    # step 5: a predicted time for n = 1024 (SPEC.md cli example)
+    kf = sorted(p for p in (tmp_path / "k").iterdir() if p.name.startswith("matmul_sq"))[0]
+    t = float(run("predict", "--model", "cal.json", "--kernel", kf, "--bind", "n=1024",
+                  cwd=tmp_path).stdout)
+    from paper_1904_09538_b200 import host
+    vid = kf.stem.replace("n-2048", "n-1024")
+    f = host.HostModel(MODEL).feature_table([vid])[0]
+    exact = 2e-13 * f[0] + 3e-12 * f[1] + 5e-6 * f[2]
+    assert abs(t - exact) <= 1e-9 * exact
+    # report: per-variant series, geomean table, a ranking row per size
+    rank = list(csv.reader(l for l in open(tmp_path / "rep" / "ranking.csv") if not l.startswith("#")))
+    assert rank[0] == ["size", "measured_winner", "predicted_winner", "correct"]
+    assert len(rank) == 5 and all(r[3] == "yes" for r in rank[1:])
+    summ = (tmp_path / "rep" / "summary.csv").read_text()
+    assert "\noverall," in summ
+    series = (tmp_path / "rep" / "series.csv").read_text().splitlines()
+    assert series[1] == "variant,size,measured_seconds,predicted_seconds" and len(series) == 10
+
+
+def test_byte_identical_reruns(cli, tmp_path):
+    a, b = tmp_path / "a", tmp_path / "b"
+    a.mkdir()
+    b.mkdir()
+    env = {"SOURCE_DATE_EPOCH": "1700000000"}
+    pipeline(a, env)
+    pipeline(b, env)
+    files = sorted(p.relative_to(a) for p in a.rglob("*") if p.is_file())
+    assert len(files) > 10
+    for rel in files:
+        assert (a / rel).read_bytes() == (b / rel).read_bytes(), rel
+
+
+def test_error_exit_codes(cli, tmp_path):
+    pipeline(tmp_path)
+    kf = sorted(p for p in (tmp_path / "k").iterdir() if p.name.startswith("matmul_sq"))[0]
+    r = run("predict", "--model", "cal.json", "--kernel", kf, "--bind", "n=1000", cwd=tmp_path,
+            check=False)
+    assert r.returncode == 1 and "violates assumption n mod 16 == 0" in r.stderr
+    # one measured row for a three-parameter model: rank deficient
+    lines = (tmp_path / "meas.csv").read_text().splitlines()
+    hdr = [i for i, l in enumerate(lines) if l.startswith("kernel,")][0]
+    (tmp_path / "one.csv").write_text("\n".join(lines[: hdr + 2]) + "\n")
+    r = run("calibrate", "--model", "m.txt", "--features", "f.csv", "--measurements", "one.csv",
+            "--out", "x.json", cwd=tmp_path, check=False)
+    assert r.returncode == 1 and r.stderr.startswith("error:")
+    r = run("measure", "--kernels", "k", "--out", "x.csv", cwd=tmp_path, check=False)
+    assert r.returncode == 1 and "--device is required" in r.stderr
+
+
+@pytest.mark.gpu
+def test_measure_on_b200(cli, tmp_path):
+    run("generate", "--catalog", "b200", "--tag", "matmul_sq_rm", "--tag", "n:1024",
+        "--tag", "prefetch:True", "--out", "k", cwd=tmp_path)
+    run("measure", "--device", "cuda:0", "--kernels", "k", "--trials", 10, "--warmup", 2,
+        "--out", "meas.csv", cwd=tmp_path)
+    lines = (tmp_path / "meas.csv").read_text().splitlines()
+    assert lines[1] == "# device: cuda_b200_0, trials: 10"
+    rows = list(csv.DictReader(l for l in lines if not l.startswith("#")))
+    assert len(rows) == 2 and all(0 < float(r["mean_seconds"]) < 1 for r in rows)
