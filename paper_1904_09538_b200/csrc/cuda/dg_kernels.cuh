@@ -30,27 +30,64 @@ __device__ __forceinline__ int64_t dg_res_idx(bool trans, const DgDims& d, int m
   return trans ? ((int64_t)m * d.np + i) * d.nel + k : ((int64_t)m * d.nel + k) * d.np + i;
 }
 
+// Lane skew of the u-row loads (noPF, dmPF and their work-removed kernels).
+// A work-item reads its own u row k (pitch Np floats) 32 bytes at a time; the
+// 16 k of a warp sit Np*4 bytes apart, so when that pitch is a multiple of
+// 128 B every lane's sector of one load instruction lies at the same offset
+// within its cache line, and the warp's 16 sectors are served one per L1
+// cycle (measured on B200: Np = 32, 64, 96, 128 run at ~3.4 TF/s, Np = 16, 48
+// — pitch an odd multiple of 64 B — at ~5 TF/s). Skewing which chunk a lane
+// loads in a given instruction spreads the sectors over 4 (2 for dmPF) line
+// offsets. Only the issue schedule changes: each work-item still loads the
+// same elements and accumulates them in the same order.
+//   pitch % 128 == 0  (Np/8 % 4 == 0): skew = lx & 3, offsets 0..3 from the skew
+//   pitch % 128 == 64 (Np/8 % 4 == 2): skew = (lx >> 1) & 1, the row parity
+//                                      supplies the other factor of 2
+__device__ __forceinline__ int dg_lane_skew(int lx, int nj8, int* smax) {
+  const bool four = (nj8 & 3) == 0;
+  *smax = four ? 3 : 1;
+  return four ? (lx & 3) : ((lx >> 1) & 1);
+}
+// dmPF: a tile's u row is two 32-byte chunks; half the lanes load them in
+// reverse order (2 line offsets, 4 with the row parity when Np/8 % 4 == 2).
+__device__ __forceinline__ bool dg_lane_swap(int lx, int nj8) {
+  return ((nj8 & 3) == 0) ? (lx & 1) : ((lx >> 1) & 1);
+}
+
 // noPF: no local memory; m outermost, reduction over j. The work-item's own
 // row reads along the sequential j are issued as 32-byte loads (Np is a
 // multiple of 16, so rows are 64-byte aligned): the same thread reads the same
-// elements and accumulates them in the same order, in an eighth of the load
-// instructions (each warp-wide u load touches 16 rows either way).
+// elements and accumulates them in the same order. The (m, j8) chunk sequence
+// of a work-item runs as one stream, lane l starting dg_lane_skew(l) steps
+// late; a work-item stores res[m, k, i] when its m-th row completes.
 __global__ void __launch_bounds__(256) dg_nopf(const float* __restrict__ dm,
                                                const float* __restrict__ u,
                                                float* __restrict__ res, DgDims d) {
-  const int64_t k = (int64_t)blockIdx.x * 16 + threadIdx.x;
-  const int i = blockIdx.y * 16 + threadIdx.y;
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int64_t k = (int64_t)blockIdx.x * 16 + lx;
+  const int i = blockIdx.y * 16 + ly;
+  const int nj8 = d.np / 8;
+  int smax;
+  const int s = dg_lane_skew(lx, nj8, &smax);
+  const int S = d.nmat * nj8;
   const float* urow = u + k * d.np;
-  for (int m = 0; m < d.nmat; ++m) {
-    const float* dmrow = dm + ((int64_t)m * d.np + i) * d.np;
-    float acc = 0.f;
-#pragma unroll 2
-    for (int j8 = 0; j8 < d.np / 8; ++j8) {
+  const float* dmrow = dm + (int64_t)i * d.np;
+  int m = 0, j8 = 0;
+  float acc = 0.f;
+  for (int t = 0; t < S + smax; ++t) {
+    const int c = t - s;
+    if (c >= 0 && c < S) {
       const f8 a = ldg256(dmrow + 8 * j8), b = ldg256(urow + 8 * j8);
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc = __fmaf_rn(a.v[q], b.v[q], acc);
+      if (++j8 == nj8) {
+        res[dg_res_idx(false, d, m, k, i)] = acc;
+        acc = 0.f;
+        j8 = 0;
+        ++m;
+        dmrow += (int64_t)d.np * d.np;
+      }
     }
-    res[dg_res_idx(false, d, m, k, i)] = acc;
   }
 }
 
@@ -103,8 +140,9 @@ __global__ void __launch_bounds__(256) dg_upf(const float* __restrict__ dm,
 // memory (two barriers per tile); u read directly (strided by Np in dmPF,
 // unit-stride across lid(0) in the transposed layout). The work-item's
 // dm_fetch row is read 4 j_in at a time (LDS.128, pitch 20), and in dmPF its
-// u row 8 at a time (32-byte loads); all 16 u loads of a j_out tile are issued
-// before its FMAs, which run in j_in order.
+// u row 8 at a time (32-byte loads, the two chunks of a tile in lane-swapped
+// order, dg_lane_swap); all 16 u loads of a j_out tile are issued before its
+// FMAs, which run in j_in order.
 template <bool TRANS>
 __global__ void __launch_bounds__(256) dg_dmpf(const float* __restrict__ dm,
                                                const float* __restrict__ u,
@@ -113,6 +151,7 @@ __global__ void __launch_bounds__(256) dg_dmpf(const float* __restrict__ dm,
   const int lx = threadIdx.x, ly = threadIdx.y;
   const int64_t k = (int64_t)blockIdx.x * 16 + lx;
   const int i0 = blockIdx.y * 16;
+  const bool sw = !TRANS && dg_lane_swap(lx, d.np / 8);
   for (int m = 0; m < d.nmat; ++m) {
     float acc = 0.f;
     for (int jo = 0; jo < d.np / 16; ++jo) {
@@ -134,7 +173,14 @@ __global__ void __launch_bounds__(256) dg_dmpf(const float* __restrict__ dm,
           acc = __fmaf_rn(a.w, b3, acc);
         }
       } else {
-        const f8 b0 = ldg256(u + k * d.np + jo * 16), b1 = ldg256(u + k * d.np + jo * 16 + 8);
+        const float* ur = u + k * d.np + jo * 16;
+        const f8 x0 = ldg256(ur + (sw ? 8 : 0)), x1 = ldg256(ur + (sw ? 0 : 8));
+        f8 b0, b1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          b0.v[q] = sw ? x1.v[q] : x0.v[q];
+          b1.v[q] = sw ? x0.v[q] : x1.v[q];
+        }
 #pragma unroll
         for (int j4 = 0; j4 < 4; ++j4) {
           const float4 a = *reinterpret_cast<const float4*>(&dmf[ly][4 * j4]);
@@ -180,14 +226,25 @@ __global__ void __launch_bounds__(256) dg_rm(const float* __restrict__ src,
       acc = __fadd_rn(acc, v.w);
     };
     if constexpr (VARIANT == 0) {
-      // statement within (m, k, i), reduction j
-      for (int m = 0; m < d.nmat; ++m) {
-        const float* row = KEEP == 3 ? src + k * d.np : src + ((int64_t)m * d.np + i) * d.np;
-#pragma unroll 2
-        for (int j8 = 0; j8 < d.np / 8; ++j8) {
+      // statement within (m, k, i), reduction j; the application kernel's
+      // lane-skewed (m, j8) chunk stream
+      const int nj8 = d.np / 8;
+      int smax;
+      const int s = dg_lane_skew(lx, nj8, &smax);
+      const int S = d.nmat * nj8;
+      const float* row0 = KEEP == 3 ? src + k * d.np : src + (int64_t)i * d.np;
+      const float* row = row0;
+      int j8 = 0;
+      for (int t = 0; t < S + smax; ++t) {
+        const int c = t - s;
+        if (c >= 0 && c < S) {
           const f8 v = ldg256(row + 8 * j8);
 #pragma unroll
           for (int q = 0; q < 8; ++q) acc = __fadd_rn(acc, v.v[q]);
+          if (++j8 == nj8) {
+            j8 = 0;
+            if (KEEP != 3) row += (int64_t)d.np * d.np;
+          }
         }
       }
     } else if constexpr (VARIANT == 1) {
@@ -221,11 +278,13 @@ __global__ void __launch_bounds__(256) dg_rm(const float* __restrict__ src,
                 for (int q = 0; q < 4; ++q)
                   acc = __fadd_rn(acc, src[dg_u_idx(true, d, k, jo * 16 + 4 * j4 + q)]);
             } else {
-              const f8 b0 = ldg256(src + k * d.np + jo * 16), b1 = ldg256(src + k * d.np + jo * 16 + 8);
+              const bool sw = dg_lane_swap(lx, d.np / 8);
+              const float* ur = src + k * d.np + jo * 16;
+              const f8 x0 = ldg256(ur + (sw ? 8 : 0)), x1 = ldg256(ur + (sw ? 0 : 8));
 #pragma unroll
-              for (int q = 0; q < 8; ++q) acc = __fadd_rn(acc, b0.v[q]);
+              for (int q = 0; q < 8; ++q) acc = __fadd_rn(acc, sw ? x1.v[q] : x0.v[q]);
 #pragma unroll
-              for (int q = 0; q < 8; ++q) acc = __fadd_rn(acc, b1.v[q]);
+              for (int q = 0; q < 8; ++q) acc = __fadd_rn(acc, sw ? x0.v[q] : x1.v[q]);
             }
           }
       } else {

@@ -610,11 +610,17 @@ GeneratedKernel make_dg_diff(const ArgMap& args) {
              ld("u", {times(16, I("k_out")) + I("i_in"), times(16, I("j_out")) + I("k_in")}, "dg-uPF-u"),
              with({"j_out"}), {"bar_pre"});
     b.barrier("bar_post", with({"j_out"}), {"fetch"});
+    // u_fetch[k_in, j_in] is invariant in the innermost m loop: it is read
+    // once per (j_out, j_in) into a private value and reused for the nmat
+    // accumulators (as any compiler hoists it, and as the sm_100a kernel does),
+    // so local loads count Np per work-item, not nmat * Np.
+    b.array("u_val", dt, {}, MemSpace::private_mem);
+    b.assign("u_read", Access{"u_val", "", {}}, ld("u_fetch", {I("k_in"), I("j_in")}),
+             with({"j_out", "j_in"}), {"bar_post"});
     b.assign("update", Access{"acc", "", {I("m")}},
              bin(BinOp::add, ld("acc", {I("m")}),
-                 bin(BinOp::mul, ld("diff_mat", {I("m"), i, j}, "dg-uPFnoPF-dm"),
-                     ld("u_fetch", {I("k_in"), I("j_in")}))),
-             with({"j_out", "j_in", "m"}), {"bar_post"});
+                 bin(BinOp::mul, ld("diff_mat", {I("m"), i, j}, "dg-uPFnoPF-dm"), var("u_val"))),
+             with({"j_out", "j_in", "m"}), {"u_read"});
     b.assign("store", res_access("dg-uPF-res"), ld("acc", {I("m")}), with({"m"}), {"update"});
   } else {
     const AffineExpr j = times(16, I("j_out")) + I("j_in");
