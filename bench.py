@@ -111,6 +111,32 @@ class Dist:
                     out.append((int(k), int(t), s))
         return out
 
+    def all_gather_rows(self, a: np.ndarray) -> np.ndarray:
+        """All-gather a [rows, cols] float64 block per rank (rows may differ)
+        into the rank-ordered concatenation, as fixed-size padded tensors."""
+        if not self.pg:
+            return a
+        import torch
+        dev = f"cuda:{self.device}" if self.backend == "nccl" else "cpu"
+        a = np.ascontiguousarray(a, dtype=np.float64).reshape(len(a), -1)
+        n = torch.tensor([a.shape[0]], dtype=torch.int64, device=dev)
+        sizes = [torch.zeros_like(n) for _ in range(self.world)]
+        self.pg.all_gather(sizes, n)
+        sizes = [int(x.item()) for x in sizes]
+        buf = torch.zeros((max(sizes), a.shape[1]), dtype=torch.float64, device=dev)
+        buf[: a.shape[0]] = torch.from_numpy(a).to(dev)
+        parts = [torch.empty_like(buf) for _ in range(self.world)]
+        self.pg.all_gather(parts, buf)
+        return np.concatenate([p[:m].cpu().numpy() for p, m in zip(parts, sizes)])
+
+    def broadcast(self, obj):
+        """Rank 0's picklable object on every rank."""
+        if not self.pg:
+            return obj
+        box = [obj]
+        self.pg.broadcast_object_list(box, src=0)
+        return box[0]
+
     def close(self):
         if self.pg:
             self.pg.destroy_process_group()
@@ -445,19 +471,23 @@ def _concrete(vid: str, sizes: dict[str, int]) -> str:
     return "__".join([gen] + [f"{k}-{args[k]}" for k in sorted(args)])
 
 
-def c5_report(dev, parts, models: dict, heads: dict, npts: int = 1_000_000) -> dict:
-    """Every application variant of every workload, with its workload's
-    headline model and fitted parameters, evaluated at npts seeded points
-    (BASELINE.json configs[4]); winners per application. Checked against the
-    CPU port of the same tables and against the reference-API predict()."""
+def c5_block(npts: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block of the C5 points evaluated by `rank` (SURVEY 8(e):
+    10^6 points in blocks of 125k per GPU at 8 GPUs)."""
+    per = -(-npts // world)
+    return min(npts, rank * per), min(npts, (rank + 1) * per)
+
+
+def c5_variants(parts, models: dict, heads: dict) -> list[dict]:
+    """One entry per application variant: its workload's headline model,
+    fitted parameters, argmin group and size-coordinate map."""
     from paper_1904_09538_b200 import host, workloads
-    from paper_1904_09538_b200.predict import PredictionTables, c5_points
-    variants, coord_of = [], []
+    variants = []
     for g, (wl, _cal, app) in enumerate(parts):
         h = heads[wl.name]
         fit = models[wl.name].get(h["model"], {}).get(h["fit"] or "", {})
         if "params" not in fit:
-            return {"error": f"{wl.name}: no fitted parameters"}
+            raise RuntimeError(f"{wl.name}: no fitted parameters")
         m = host.HostModel(wl.models[h["model"]])
         params = [fit["params"][n] for n in m.params]
         seen = set()
@@ -468,13 +498,34 @@ def c5_report(dev, parts, models: dict, heads: dict, npts: int = 1_000_000) -> d
             seen.add(key)
             variants.append({"id": vid, "model": wl.models[h["model"]], "params": params,
                              "group": g, "coords": wl.c5_coords})
-            coord_of.append(wl.c5_coords)
+    return variants
+
+
+def c5_report(dev, parts, variants: list[dict], npts: int = 1_000_000, dist=None) -> dict | None:
+    """Every application variant of every workload, with its workload's
+    headline model and fitted parameters, evaluated at npts seeded points
+    (BASELINE.json configs[4]); winners per application. Each rank evaluates
+    one contiguous block of points (c5_block); predictions and argmins are
+    all-gathered (NCCL over NVLink on GPUs) and rank 0 checks them against
+    the CPU port of the same tables and against the reference-API predict()."""
+    from paper_1904_09538_b200 import host, workloads
+    from paper_1904_09538_b200.predict import PredictionTables, c5_points
+    rank, world = (dist.rank, dist.world) if dist else (0, 1)
     t = PredictionTables(variants)
     pts = c5_points(npts)
-    t.eval_gpu(dev, pts[:4096])  # warm
+    lo, hi = c5_block(npts, rank, world)
+    t.eval_gpu(dev, pts[lo:lo + max(1, min(4096, hi - lo))])  # warm
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
-    pg, ag, ksec = t.eval_gpu(dev, pts)
+    pg, ag, ksec = t.eval_gpu(dev, pts[lo:hi])
     wall = time.perf_counter() - t0
+    if dist and dist.world > 1:
+        pg = dist.all_gather_rows(pg)
+        ag = dist.all_gather_rows(ag.astype(np.float64)).astype(np.int64)
+        ksec, wall = dist.max(ksec), dist.max(wall)
+    if rank != 0:
+        return None
     nsub = min(npts, 100_000)
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
@@ -506,7 +557,8 @@ def c5_report(dev, parts, models: dict, heads: dict, npts: int = 1_000_000) -> d
         winners[wl.name] = {workloads.variant_of(variants[i]["id"], wl.variant_keys): int(cnt[i])
                             for i in cols}
     nev = npts * t.nvar
-    return {"points": npts, "variants": t.nvar, "evaluations": nev,
+    return {"points": npts, "variants": t.nvar, "evaluations": nev, "ranks": world,
+            "points_per_rank": hi - lo,
             "gpu_kernel_ms": round(ksec * 1e3, 3),
             "gpu_evals_per_s": round(nev / ksec, 1),
             "gpu_e2e_ms": round(wall * 1e3, 2), "gpu_e2e_evals_per_s": round(nev / wall, 1),
@@ -699,11 +751,7 @@ def run_ours(args, dist: Dist) -> None:
         for a in ins + outs:
             a.free()
 
-    if dist.rank != 0:
-        dev.close()
-        return
-
-    # ----- measurement table -> summaries -----
+    # ----- measurement table -> summaries (every rank holds the gathered table) -----
     trials: dict[int, list[float]] = {}
     for k, _t, s in table:
         trials.setdefault(k, []).append(s)
@@ -766,28 +814,39 @@ def run_ours(args, dist: Dist) -> None:
     gm = [k for k in trials if descs[k].gen == 1]
     roofline_hbm = roofline_of(max(gm, key=lambda k: ios[k].bytes_global)) if gm else None
 
-    if args.table:
+    if args.table and dist.rank == 0:
         # measurements_to_csv format (executor.cpp:279-295) + raw trials
         with open(args.table, "w") as f:
             f.write("kernel,bindings,mean_seconds,trials,raw\n")
             for k, ts in sorted(trials.items()):
                 m, kept = summarize(ts)
                 f.write(f"{kernels[k]},,{m!r},{kept},{' '.join(repr(x) for x in ts)}\n")
+    # the fit runs once (rank 0); its headline parameters go to every rank
     models, heads = {}, {}
-    for wl, cal, app in parts:
-        models[wl.name] = model_report(wl, cal, app, mean_s, dev)
-        hmodel = args.headline_model if args.headline_model in wl.models else wl.headline_model
-        hfit, head = headline(models[wl.name], hmodel)
-        heads[wl.name] = {"model": hmodel, "fit": hfit,
-                          "geomean_rel_error": head.get("geomean_rel_error"),
-                          "geomean_rel_error_all": head.get("geomean_rel_error_all"),
-                          "ranking_correct": head.get("ranking_correct"),
-                          "ranking_correct_gap_ge_2pct": head.get("ranking_correct_gap_ge_2pct")}
+    if dist.rank == 0:
+        for wl, cal, app in parts:
+            models[wl.name] = model_report(wl, cal, app, mean_s, dev)
+            hmodel = args.headline_model if args.headline_model in wl.models else wl.headline_model
+            hfit, head = headline(models[wl.name], hmodel)
+            heads[wl.name] = {"model": hmodel, "fit": hfit,
+                              "geomean_rel_error": head.get("geomean_rel_error"),
+                              "geomean_rel_error_all": head.get("geomean_rel_error_all"),
+                              "ranking_correct": head.get("ranking_correct"),
+                              "ranking_correct_gap_ge_2pct": head.get("ranking_correct_gap_ge_2pct")}
     try:
-        model_eval = (c5_report(dev, parts, models, heads, args.c5_points)
-                      if args.c5_points else None)
+        variants = c5_variants(parts, models, heads) if dist.rank == 0 else None
+        err = None
+    except Exception as e:  # reported, not hidden
+        variants, err = None, str(e)
+    variants, err = dist.broadcast((variants, err))
+    try:
+        model_eval = (c5_report(dev, parts, variants, args.c5_points, dist)
+                      if args.c5_points and variants else ({"error": err} if err else None))
     except Exception as e:  # reported, not hidden
         model_eval = {"error": str(e)}
+    if dist.rank != 0:
+        dev.close()
+        return
     try:
         diagnosis = overlap_diagnosis(parts, models, mean_s)
     except Exception as e:

@@ -94,6 +94,23 @@ def lsu_model(gmem: list[tuple[str, str]], ops: list[tuple[str, str]],
     return OUTPUT + "\n" + ovh + " + " + sharp_max(cmem, sharp_max(cops, cb, k), k) + "\n"
 
 
+def lsu2_model(hbm: list[tuple[str, str]], tags: list[tuple[str, str]],
+               ops: list[tuple[str, str]], lmem: list[tuple[str, str]], k: float = 40.0) -> str:
+    """launch/group overhead + max(c_hbm, c_tags + c_lmem, c_ops, c_barrier):
+    the generic AFR-1 streams (G16/G18) calibrated by the HBM
+    microbenchmarks are DRAM-bandwidth cost and overlap everything on chip;
+    the tagged application accesses (mostly L1/L2 hits, each calibrated by
+    its work-removed kernel) share the LSU/MIO pipe with shared-memory
+    accesses, so those two add; the FP32 pipe and barriers overlap both."""
+    ovh = _sum([f"p_group * {GROUPS}", f"p_launch * {LAUNCH}"])
+    ch = _sum([f"{p} * {f}" for p, f in hbm])
+    cl = _sum([f"{p} * {f}" for p, f in tags] + [f"{p} * {f}" for p, f in lmem])
+    cops = _sum([f"{p} * {f}" for p, f in ops])
+    cb = f"p_bar * {BAR} * {GROUPS}"
+    return (OUTPUT + "\n" + ovh + " + " +
+            sharp_max(ch, sharp_max(cl, sharp_max(cops, cb, k), k), k) + "\n")
+
+
 def overlap3_model(gmem: list[tuple[str, str]], ops: list[tuple[str, str]],
                    lmem: list[tuple[str, str]]) -> str:
     """ovh + max(c_gmem, max(c_ops, c_lmem)): the paper's overlap form with the
@@ -150,7 +167,8 @@ MATMUL = Workload(
             "nonlinear": overlap_model(MATMUL_GMEM, ONCHIP),
             "overlap3": overlap3_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:]),
             "max3": max3_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:]),
-            "lsu": lsu_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:])},
+            "lsu": lsu_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:]),
+            "lsu2": lsu2_model(MATMUL_GMEM[:1], MATMUL_GMEM[1:], ONCHIP[:3], ONCHIP[3:])},
     variant_keys=("prefetch",),
     size_keys=("n",),
 )
@@ -170,7 +188,8 @@ FD = Workload(
     application_tags=[["finite_diff"]],
     models={"linear": linear_model(FD_GMEM, ONCHIP),
             "max3": max3_model(FD_GMEM, ONCHIP[:3], ONCHIP[3:]),
-            "lsu": lsu_model(FD_GMEM, ONCHIP[:3], ONCHIP[3:])},
+            "lsu": lsu_model(FD_GMEM, ONCHIP[:3], ONCHIP[3:]),
+            "lsu2": lsu2_model(FD_GMEM[:2], FD_GMEM[2:], ONCHIP[:3], ONCHIP[3:])},
     variant_keys=("tile",),
     size_keys=("n",),
     extra={"options": {"partial_subgroups": "round_up"}},
@@ -192,7 +211,8 @@ DG = Workload(
     application_tags=[["dg_diff"]],
     models={"linear": linear_model(DG_GMEM, ONCHIP),
             "max3": max3_model(DG_GMEM, ONCHIP[:3], ONCHIP[3:]),
-            "lsu": lsu_model(DG_GMEM, ONCHIP[:3], ONCHIP[3:])},
+            "lsu": lsu_model(DG_GMEM, ONCHIP[:3], ONCHIP[3:]),
+            "lsu2": lsu2_model(DG_GMEM[:1], DG_GMEM[1:], ONCHIP[:3], ONCHIP[3:])},
     variant_keys=("variant",),
     size_keys=("nelements", "nunit_nodes"),
     c5_coords={"nelements": 2, "nunit_nodes": 3},

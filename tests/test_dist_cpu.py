@@ -37,7 +37,26 @@ def _worker(rank: int, world: int, port: int, q) -> None:
         load = sum(est[i] for i, _ in mine)
         mx = dist.max(load)
         dist.barrier()
-        q.put((rank, len(mine), sorted(table), load, mx, len(units)))
+        # C5 prediction sharding: contiguous point blocks per rank, predictions
+        # and argmins all-gathered; the fitted variants come from rank 0
+        import numpy as np
+        from paper_1904_09538_b200.predict import PredictionTables, c5_points
+        model = ("f_exec_wall_time_cuda_b200_0\n"
+                 "p_launch * f_sync_kernel_launch + p_madd * f_op_float32_madd"
+                 " + p_l * f_mem_access_local_float32\n")
+        base = "matmul_sq__dtype-float32__groups_fit-True__lsize_0-16__lsize_1-16__n-512__prefetch-"
+        variants = [{"id": base + pf, "model": model, "params": [5e-6, 1e-12 * (1 + i), 2e-12],
+                     "group": 0, "coords": {"n": 0}} for i, pf in enumerate(("True", "False"))]
+        variants = dist.broadcast(variants if rank == 0 else None)
+        t = PredictionTables(variants)
+        pts = c5_points(1001)
+        lo, hi = bench.c5_block(len(pts), rank, world)
+        p, a = t.eval_cpu(pts[lo:hi])
+        P = dist.all_gather_rows(p)
+        A = dist.all_gather_rows(a.astype(np.float64)).astype(np.int64)
+        fp, fa = t.eval_cpu(pts)
+        c5 = (hi - lo, bool(np.array_equal(P, fp)), bool(np.array_equal(A, fa.astype(np.int64))))
+        q.put((rank, len(mine), sorted(table), load, mx, len(units), c5))
         dist.close()
     except Exception as e:  # surfaced by the parent
         q.put((rank, "error", repr(e)))
@@ -80,3 +99,12 @@ def test_max_over_ranks_and_lpt_balance(results):
     assert results[0][4] == results[1][4] == max(loads)
     # LPT: the makespan is within one largest unit of the perfect split
     assert max(loads) - min(loads) <= max(loads) * 0.5
+
+
+def test_c5_points_sharded_and_gathered(results):
+    # 10^6 points in contiguous per-rank blocks, one all-gather
+    n0, n1 = results[0][6][0], results[1][6][0]
+    assert n0 + n1 == 1001 and abs(n0 - n1) <= 1
+    for r in (0, 1):
+        assert results[r][6][1], "gathered predictions equal the single-rank evaluation"
+        assert results[r][6][2], "gathered argmins equal the single-rank evaluation"

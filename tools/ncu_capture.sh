@@ -17,6 +17,8 @@ cap mm_nopf_8192 matmul_nopf "matmul_sq__dtype-float32__groups_fit-True__lsize_0
 cap mm_pf_4096 matmul_pf "matmul_sq__dtype-float32__groups_fit-True__lsize_0-16__lsize_1-16__n-4096__prefetch-True"
 cap fd16_8176 finite_diff_strip "finite_diff__dtype-float32__n-8176__tile-16x16"
 cap dg_upf_1e6 dg_upf "dg_diff__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-64__variant-uPF"
+cap dg_nopf_1e6 dg_nopf "dg_diff__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-64__variant-noPF"
+cap dg_dmpf_1e6 dg_dmpf "dg_diff__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-64__variant-dmPF"
 cap dg_dmpft_1e6 dg_dmpf "dg_diff__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-64__variant-dmPFtrans"
 cap madd flops_pattern "flops_madd_pattern__dtype-float32__lid_stride_0-1__lid_stride_1-2048__lsize_0-16__lsize_1-16__m-128__nelements-2097152"
 cap tc_8192 matmul_tc_kernel "matmul_sq_tc__dtype-float32__lsize_0-16__lsize_1-16__n-8192"
