@@ -36,3 +36,12 @@ $(OUT)/port_extra: $(ROOT)/tests/port_extra.cpp $(LIB)
 
 extra: $(OUT)/port_extra
 .PHONY: extra
+
+# SPEC acceptance criteria 1-11 against the port (uses the reference's test
+# support header, read in place, for its random-kernel generator).
+$(OUT)/port_acceptance: $(ROOT)/tests/acceptance.cpp $(LIB)
+	@mkdir -p $(OUT)
+	$(CXX) $(CXXFLAGS) $< -L$(dir $(LIB)) -lperfseer_b200 -Wl,-rpath,$(dir $(LIB)) -o $@
+
+acceptance: $(OUT)/port_acceptance
+.PHONY: acceptance
