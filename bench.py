@@ -574,6 +574,20 @@ def c5_report(dev, parts, variants: list[dict], npts: int = 1_000_000, dist=None
 # CPU baseline: the oracle restatement (oracle/suite_ref.c) on host cores
 
 
+def reference_model_sample(seconds: float = 2.0) -> dict:
+    """The unmodified reference library (oracle/_ref, compiled from
+    /root/reference by oracle/Makefile; travels prebuilt) timed on the host
+    cores for the modelling half of the path: analyze, gather_feature_values,
+    fit_model and predict (oracle/ref_cpu_bench.cpp)."""
+    exe = ROOT / "oracle" / "_ref" / "ref_cpu_bench"
+    if not exe.exists():
+        return {"unavailable": "oracle/_ref/ref_cpu_bench not built (needs /root/reference at build time)"}
+    r = subprocess.run([str(exe), str(seconds)], capture_output=True, text=True, timeout=300)
+    if r.returncode != 0:
+        return {"error": r.stderr.strip()[-300:]}
+    return json.loads(r.stdout)
+
+
 def cpu_gmem_sample(elements: int = 1 << 26, reps: int = 3) -> dict:
     from oracle import suite as oracle_suite
     from paper_1904_09538_b200 import desc_from_id, kernel_io
@@ -889,6 +903,8 @@ def run_ours(args, dist: Dist) -> None:
         "overlap_diagnosis": diagnosis,
         "roofline_hbm": roofline_hbm,
         "cpu_baseline": cpu_gmem_sample() if dist.world == 1 else None,
+        # the reference library itself on the host cores (modelling path)
+        "cpu_baseline_reference": reference_model_sample() if dist.world == 1 else None,
         "e2e": {"value": round(e2e_bytes_all / e2e_time_max / 1e9, 3) if e2e_time_max else None,
                 "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "kernels": len(e2e_set), "note": "ps_run_host: pinned host in, H2D + kernel + D2H"},

@@ -42,3 +42,17 @@ def test_port_reproduces_reference_goldens_byte_for_byte(built):
     assert r.returncode == 0, r.stderr.decode()
     golden = (ROOT / "tests" / "golden" / "reference.json").read_bytes()
     assert r.stdout == golden
+
+
+def test_reference_cpu_baseline_runs():
+    # the bench's cpu_baseline_reference: the unmodified reference library timed
+    # on the host (oracle/ref_cpu_bench.cpp)
+    import json
+    subprocess.run(["make", "-C", str(ROOT / "oracle"), "_ref/ref_cpu_bench"], check=True,
+                   capture_output=True)
+    r = subprocess.run([str(ROOT / "oracle" / "_ref" / "ref_cpu_bench"), "0.2", "2"],
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    j = json.loads(r.stdout)
+    assert j["kind"] == "reference" and j["threads"] == 2 and j["catalog_kernels"] == 172
+    assert j["predict_evals_per_s"] > 0 and j["fits_per_s"] > 0 and j["analyze_kernels_per_s"] > 0
