@@ -9,16 +9,19 @@
 // oracle bit for bit; on U[-1,1) inputs the TF32 operand rounding bounds the
 // error (stated in tests/test_gpu_parity.py).
 //
-// kind::tf32 takes K-major operands only (a transposed, N-major B is
-// silently ignored by the tensor core — measured on B200), so each launch
-// first writes Bt = B^T (n x n, coalesced 32x32 smem tiles, ~2 x 4n^2 bytes
-// of HBM traffic) and the GEMM reads A and Bt both K-major. The transpose is
-// part of the variant and inside the timed launch.
+// A is read K-major (row-major A[m][k]); B is read N-major straight from
+// row-major B[k][n] (instruction descriptor b_major = MN). For tf32 the only
+// MN-major shared-memory layout the tensor core accepts is the 128-byte
+// swizzle with 32-byte atomicity (SWIZZLE_128B_BASE32B, TMA
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B; with the plain 128-byte swizzle the
+// accumulator silently stays zero — measured). PS_TC_B=k selects the older
+// path that first writes Bt = B^T and reads both operands K-major (~11% slower
+// at n = 8192: 0.2 ms of transpose traffic per launch).
 //
 // Persistent CTAs (one per SM) over 128x256 output tiles, 6 warps:
-//   warp 0 lane 0  TMA producer: per 32-wide K block, A 128x32 and Bt 256x32
-//                  (both K-major, one box each) into a 4-stage ring,
-//                  128-byte swizzle, mbarrier complete_tx;
+//   warp 0 lane 0  TMA producer: per 32-wide K block, A 128x32 (K-major) and
+//                  B 32x256 (N-major, one 3-D box) into a 4-stage ring,
+//                  mbarrier complete_tx;
 //   warp 1 lane 0  MMA issuer: 4 x tcgen05.mma (M=128, N=256, K=8) per stage
 //                  into one of two TMEM accumulators, tcgen05.commit frees
 //                  the stage / publishes the accumulator;
@@ -28,7 +31,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "runtime_internal.h"
 
@@ -48,6 +53,8 @@ constexpr uint32_t TMEM_COLS = 256;         // 128 lanes x 256 fp32 columns
 // D f32, A/B tf32, both K-major, N>>3 at bit 17, M>>4 at bit 24.
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (0u << 16) |
                            (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+// Same with B N-major (b_major bit 16): B read straight from row-major [k][n].
+constexpr uint32_t IDESC_BMN = IDESC | (1u << 16);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -89,13 +96,31 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uin
          (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+// MN-major tf32 operands take the 128-byte swizzle with 32-byte atomicity
+// (layout type 1, SWIZZLE_128B_BASE32B; cute Layout_MN_SW128_32B_Atom: rows of
+// 128 B along N, 4-row K groups of 512 B, Swizzle<2,5,2>).
+__device__ __forceinline__ uint64_t desc_sw128_32b(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(1) << 61);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc,
+                                         uint32_t idesc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n}\n" ::"r"(
           tmem_d),
-      "l"(da), "l"(db), "r"(IDESC), "r"(acc), "r"(0u)  // no output lanes disabled
+      "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(0u)  // no output lanes disabled
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
       : "memory");
 }
 
@@ -133,6 +158,11 @@ __device__ __forceinline__ void tile_coords(int t, int mt, int& m0, int& n0) {
   n0 = (band * TILE_BAND + r / mt) * BN;
 }
 
+// BMN: B is loaded N-major straight from row-major B[k][n] — one 3-D TMA box
+// of 8 N-atoms x 32 k-rows x 32 n (128 B rows, 128B swizzle with 32-byte
+// atomicity, the only MN-major layout tf32 accepts), atoms 4 KB apart (LBO),
+// 4-row K groups 512 B apart (SBO), start + 1024 B per 8-deep K step.
+template <bool BMN>
 __global__ void __launch_bounds__(192, 1)
     matmul_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      float* __restrict__ C, int n) {
@@ -184,7 +214,10 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t fb = full0 + 8 * s;
           mbar_expect_tx(fb, STAGE_BYTES);
           tma_load_2d(smem_u32(sa + s * A_BYTES), &tmA, fb, kb * BK, m0);
-          tma_load_2d(smem_u32(sb + s * B_BYTES), &tmB, fb, kb * BK, n0);
+          if constexpr (BMN)
+            tma_load_3d(smem_u32(sb + s * B_BYTES), &tmB, fb, 0, kb * BK, n0 / 32);
+          else
+            tma_load_2d(smem_u32(sb + s * B_BYTES), &tmB, fb, kb * BK, n0);
         }
       }
     }
@@ -206,8 +239,15 @@ __global__ void __launch_bounds__(192, 1)
             // K-major, 128 B swizzle rows: advance 8 tf32 (32 B) inside the
             // row; 8-row groups 1024 B apart (SBO); LBO unused (16 B)
             const uint64_t da = desc_sw128(a_base + ks * UMMA_K * 4, 16, 1024);
-            const uint64_t db = desc_sw128(b_base + ks * UMMA_K * 4, 16, 1024);
-            mma_tf32(d, da, db, (kb | ks) != 0);
+            if constexpr (BMN) {
+              // N-major: 32-n atoms 4096 B apart (LBO), 4-row K groups 512 B
+              // apart (SBO); one K step of 8 rows starts 1024 B further
+              const uint64_t db = desc_sw128_32b(b_base + ks * 1024, 4096, 512);
+              mma_tf32(d, da, db, (kb | ks) != 0, IDESC_BMN);
+            } else {
+              const uint64_t db = desc_sw128(b_base + ks * UMMA_K * 4, 16, 1024);
+              mma_tf32(d, da, db, (kb | ks) != 0, IDESC);
+            }
           }
           mma_commit(empty0 + 8 * s);  // stage s free once these MMAs have read it
         }
@@ -294,6 +334,27 @@ int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, uint3
   return PS_OK;
 }
 
+// B[k][n] row-major viewed as 3-D (32 n, k, n/32 atoms) for N-major boxes.
+int make_map_bmn(CUtensorMap* m, const void* base, int64_t n) {
+  auto fn = encode_fn();
+  if (!fn) return set_error(PS_ERR_CUDA, "matmul_sq_tc: cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {32, cuuint64_t(n), cuuint64_t(n / 32)};
+  const cuuint64_t strides[2] = {cuuint64_t(n) * 4, 128};
+  const cuuint32_t box[3] = {32, BK, BN / 32};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(PS_ERR_CUDA, "matmul_sq_tc: cuTensorMapEncodeTiled (B N-major) failed (%d)", int(r));
+  return PS_OK;
+}
+
+bool b_n_major() {
+  const char* e = std::getenv("PS_TC_B");
+  return !(e && std::string(e) == "k");
+}
+
 }  // namespace
 
 int tc_launch(Ctx* c, const ps_kernel_desc* d) {
@@ -302,20 +363,27 @@ int tc_launch(Ctx* c, const ps_kernel_desc* d) {
   if (n % BN != 0) return set_error(PS_ERR_ARG, "matmul_sq_tc requires n to be a multiple of %d", BN);
   static std::once_flag attr;
   std::call_once(attr, [] {
-    cudaFuncSetAttribute(matmul_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(matmul_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(matmul_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   });
-  DevBuf& bt = c->scratch[7];
-  if (int rc = c->ensure(bt, size_t(n) * n * sizeof(float))) return rc;
+  const int ntiles = (n / BM) * (n / BN);
+  const int grid = ntiles < c->sm_count ? ntiles : c->sm_count;
   CUtensorMap ta, tb;
   int rc = make_map(&ta, c->in[0].ptr, n, n, BK, BM);  // A [m][k]: box 32 (k) x 128 (m)
   if (rc) return rc;
+  if (b_n_major()) {
+    rc = make_map_bmn(&tb, c->in[1].ptr, n);
+    if (rc) return rc;
+    matmul_tc_kernel<true><<<grid, 192, SMEM_BYTES, c->stream>>>(ta, tb, (float*)c->out[0].ptr, n);
+    return PS_OK;
+  }
+  DevBuf& bt = c->scratch[7];
+  if (int rc2 = c->ensure(bt, size_t(n) * n * sizeof(float))) return rc2;
   rc = make_map(&tb, bt.ptr, n, n, BK, BN);            // Bt [n][k]: box 32 (k) x 256 (n)
   if (rc) return rc;
   transpose_f32<<<dim3(n / 32, n / 32), 256, 0, c->stream>>>((const float*)c->in[1].ptr,
                                                              (float*)bt.ptr, n);
-  const int ntiles = (n / BM) * (n / BN);
-  const int grid = ntiles < c->sm_count ? ntiles : c->sm_count;
-  matmul_tc_kernel<<<grid, 192, SMEM_BYTES, c->stream>>>(ta, tb, (float*)c->out[0].ptr, n);
+  matmul_tc_kernel<false><<<grid, 192, SMEM_BYTES, c->stream>>>(ta, tb, (float*)c->out[0].ptr, n);
   return PS_OK;
 }
 
