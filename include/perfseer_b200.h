@@ -160,6 +160,14 @@ int ps_buffer(ps_ctx* ctx, int is_output, int index, void** dev_ptr, int64_t* el
  * every output, bracketed by CUDA events; seconds = the whole sequence. */
 int ps_run_host(ps_ctx* ctx, const ps_kernel_desc* desc, const void* const* inputs, int n_inputs,
                 void* const* outputs, int n_outputs, double* seconds);
+/* End to end over a batch of kernels, pipelined: the H2D copies of kernel
+ * i+1, the launch of kernel i and the D2H copies of kernel i-1 overlap (three
+ * streams, two device slots; PCIe is full duplex). inputs / outputs hold, for
+ * each kernel in order, its n_inputs / n_outputs host pointers (pinned for
+ * overlap) back to back. seconds = first H2D to last D2H, CUDA events.
+ * (New; the batched form of ps_run_host for sweeps through host data.) */
+int ps_run_host_batch(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const void* const* inputs,
+                      void* const* outputs, double* seconds);
 /* Pinned host memory for ps_run_host callers. */
 int ps_host_alloc(size_t bytes, void** ptr);
 int ps_host_free(void* ptr);

@@ -787,6 +787,13 @@ int ps_destroy(ps_ctx* ctx) {
   cudaStreamSynchronize(c->stream);
   for (auto& kv : c->slots) c->release(kv.second);
   c->release(c->host_slot);
+  c->release(c->pipe_slot[0]);
+  c->release(c->pipe_slot[1]);
+  for (auto& row : c->pipe_ev)
+    for (auto e : row)
+      if (e) cudaEventDestroy(e);
+  if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+  if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
   for (auto& b : c->scratch)
     if (b.ptr) cudaFree(b.ptr);
   for (auto e : c->ev) cudaEventDestroy(e);
@@ -997,6 +1004,77 @@ int ps_run_host(ps_ctx* ctx, const ps_kernel_desc* desc, const void* const* inpu
   for (int i = 0; i < io.n_outputs; ++i)
     PS_CUDA(cudaMemcpyAsync(outputs[i], c->out[i].ptr, (size_t)io.output_elems[i] * io.elem_bytes,
                             cudaMemcpyDeviceToHost, c->stream));
+  PS_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  PS_CUDA(cudaEventSynchronize(c->ev[1]));
+  float ms = 0.f;
+  PS_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  *seconds = (double)ms * 1e-3;
+  return PS_OK;
+}
+
+int ps_run_host_batch(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const void* const* inputs,
+                      void* const* outputs, double* seconds) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !descs || !seconds || n < 0) return set_error(PS_ERR_ARG, "ps_run_host_batch: bad argument");
+  *seconds = 0.0;
+  if (n == 0) return PS_OK;
+  PS_CUDA(cudaSetDevice(c->device));
+  std::vector<ps_io_info> io(n);
+  size_t need[2][2][PS_MAX_ARRAYS] = {};  // [slot][in/out][array] bytes
+  int rc;
+  for (int i = 0; i < n; ++i) {
+    if ((rc = validate_desc(&descs[i])) || (rc = kernel_io(&descs[i], &io[i]))) return rc;
+    for (int a = 0; a < io[i].n_inputs; ++a)
+      need[i & 1][0][a] = std::max(need[i & 1][0][a], (size_t)io[i].input_elems[a] * io[i].elem_bytes);
+    for (int a = 0; a < io[i].n_outputs; ++a)
+      need[i & 1][1][a] = std::max(need[i & 1][1][a], (size_t)io[i].output_elems[a] * io[i].elem_bytes);
+  }
+  // every allocation before the timed region (cudaMalloc synchronises)
+  for (int sl = 0; sl < 2; ++sl)
+    for (int a = 0; a < PS_MAX_ARRAYS; ++a) {
+      if (need[sl][0][a] && (rc = c->ensure(c->pipe_slot[sl].in[a], need[sl][0][a]))) return rc;
+      if (need[sl][1][a] && (rc = c->ensure(c->pipe_slot[sl].out[a], need[sl][1][a]))) return rc;
+    }
+  if (!c->h2d_stream) PS_CUDA(cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking));
+  if (!c->d2h_stream) PS_CUDA(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+  for (auto& row : c->pipe_ev)
+    for (auto& e : row)
+      if (!e) PS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if ((rc = events(c, 2))) return rc;
+  cudaEvent_t(&h2d_done)[2] = c->pipe_ev[0];
+  cudaEvent_t(&run_done)[2] = c->pipe_ev[1];
+  cudaEvent_t(&d2h_done)[2] = c->pipe_ev[2];
+  c->prepared = false;
+  PS_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  PS_CUDA(cudaStreamWaitEvent(c->h2d_stream, c->ev[0], 0));
+  PS_CUDA(cudaStreamWaitEvent(c->d2h_stream, c->ev[0], 0));
+  size_t in_at = 0, out_at = 0;
+  for (int i = 0; i < n; ++i) {
+    const int sl = i & 1;
+    Slot& s = c->pipe_slot[sl];
+    // copy in once the launch two kernels back has consumed this slot's inputs
+    if (i >= 2) PS_CUDA(cudaStreamWaitEvent(c->h2d_stream, run_done[sl], 0));
+    for (int a = 0; a < io[i].n_inputs; ++a)
+      PS_CUDA(cudaMemcpyAsync(s.in[a].ptr, inputs[in_at + a], (size_t)io[i].input_elems[a] * io[i].elem_bytes,
+                              cudaMemcpyHostToDevice, c->h2d_stream));
+    PS_CUDA(cudaEventRecord(h2d_done[sl], c->h2d_stream));
+    // launch once the inputs are in and the slot's previous outputs are out
+    PS_CUDA(cudaStreamWaitEvent(c->stream, h2d_done[sl], 0));
+    if (i >= 2) PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[sl], 0));
+    s.io = io[i];
+    c->activate(s);
+    if ((rc = launch(c, &descs[i]))) return rc;
+    PS_CUDA(cudaEventRecord(run_done[sl], c->stream));
+    PS_CUDA(cudaStreamWaitEvent(c->d2h_stream, run_done[sl], 0));
+    for (int a = 0; a < io[i].n_outputs; ++a)
+      PS_CUDA(cudaMemcpyAsync(outputs[out_at + a], s.out[a].ptr, (size_t)io[i].output_elems[a] * io[i].elem_bytes,
+                              cudaMemcpyDeviceToHost, c->d2h_stream));
+    PS_CUDA(cudaEventRecord(d2h_done[sl], c->d2h_stream));
+    in_at += io[i].n_inputs;
+    out_at += io[i].n_outputs;
+  }
+  PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[(n - 1) & 1], 0));
+  if (n >= 2) PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[n & 1], 0));
   PS_CUDA(cudaEventRecord(c->ev[1], c->stream));
   PS_CUDA(cudaEventSynchronize(c->ev[1]));
   float ms = 0.f;

@@ -117,6 +117,22 @@ class CudaDevice:
         return s.value
 
 
+    def run_host_batch(self, kernels, inputs: list[list["PinnedArray"]],
+                       outputs: list[list["PinnedArray"]]) -> float:
+        """A sweep through host data, pipelined (ps_run_host_batch): H2D of the
+        next kernel, this kernel's launch and D2H of the previous one overlap;
+        seconds from the first copy in to the last copy out."""
+        ds = [_desc(k) for k in kernels]
+        arr = (_abi.KernelDesc * max(1, len(ds)))(*ds)
+        ip = [a.ptr for ins in inputs for a in ins]
+        op = [a.ptr for outs in outputs for a in outs]
+        ipa = (C.c_void_p * max(1, len(ip)))(*ip)
+        opa = (C.c_void_p * max(1, len(op)))(*op)
+        s = C.c_double()
+        check(lib().ps_run_host_batch(self._ctx, len(ds), arr, ipa, opa, C.byref(s)))
+        return s.value
+
+
 class PinnedArray:
     """Page-locked host buffer from ps_host_alloc, viewable as numpy."""
 
