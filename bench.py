@@ -685,7 +685,8 @@ def run_reference_arm(args, dist: Dist) -> None:
 BINDING = {
     7: "L1/TEX: 88% (noPF n=8192; b loads 64 B per warp per madd) / 95% (PF, LDS wavefronts); "
        "FMA pipe 14%",
-    11: "L1/TEX 88-96% (uPF, dmPFtrans), issue 79% (dmPFtrans); FMA pipe 18-21%",
+    11: "L1/TEX 96-97% (noPF, dmPF, profiles/r01_ncu_summary_dg_skew.csv), 88-96% (uPF, "
+        "dmPFtrans); FMA pipe 14-26%",
     9: "HBM 5.1 TB/s of 6.56 (dram read+write 483 MB vs 535 MB algorithmic)",
 }
 
@@ -821,7 +822,21 @@ def run_ours(args, dist: Dist) -> None:
         tf = ROOT / "profiles" / "ncu_traffic.json"
         if tf.exists():
             traffic = json.loads(tf.read_text()).get(kernels[k])
+        l1 = None
+        if d.gen == 7 and d.dtype == 0:
+            # one work-item per thread: every madd reads an a and a b operand
+            # through the L1/shared data path (global loads in noPF, a_fetch /
+            # b_fetch local loads in PF) — 8 B per madd, 8 n^3 per launch —
+            # against 148 SMs x 128 B/clk at the run's SM clock
+            ob = 8.0 * float(d.n) ** 3
+            l1_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
+            l1 = {"bound": "l1", "achieved": round(ob / avg / 1e12, 2), "peak": round(l1_peak, 2),
+                  "unit": "TB/s", "frac": round(ob / avg / 1e12 / l1_peak, 4),
+                  "operand_bytes_per_launch": ob,
+                  "basis": "IR operand loads per madd (a and b, work-item granularity) x 4 B; "
+                           "ncu l1tex throughput 88% (noPF) / 95% (PF) agrees"}
         return {"kernel": kernels[k], "bound": "fp32", "achieved": round(achieved, 3),
+                "binding_roofline": l1,
                 "peak": round(fp32_peak_tf, 2), "unit": "TFLOP/s",
                 "frac": round(achieved / fp32_peak_tf, 4), "traffic": traffic,
                 "binding_pipe": BINDING.get(d.gen),
