@@ -62,7 +62,8 @@ enum ps_generator {
   PS_GEN_FD_RM = 10,         /* make_fd_stencil_rm     uipick.cpp:641-664 */
   PS_GEN_DG = 11,            /* DG differentiation */
   PS_GEN_DG_RM = 12,         /* DG work-removed */
-  PS_GEN_MATMUL_TC = 13      /* extra: tcgen05 dense contraction (not a paper variant) */
+  PS_GEN_MATMUL_TC = 13,     /* extra: tcgen05 dense contraction (not a paper variant) */
+  PS_GEN_DG_TC = 14          /* extra: DG as a tcgen05 contraction (not a paper variant) */
 };
 
 enum ps_dtype { PS_F32 = 0, PS_F64 = 1 };

@@ -27,13 +27,15 @@ int dg_io(const ps_kernel_desc* d, ps_io_info* io) {
   const double eb = 4.0;
   auto in = [&](int64_t n) { io->input_elems[io->n_inputs++] = n; };
   auto out = [&](int64_t n) { io->output_elems[io->n_outputs++] = n; };
-  if (d->gen == PS_GEN_DG) {
+  if (d->gen == PS_GEN_DG || d->gen == PS_GEN_DG_TC) {
     in(dm);
     in(u);
     out(res);
     io->bytes_global = eb * (double)(dm + u + res);
     io->flops = 2.0 * (double)d->nmat * (double)d->nel * (double)d->np * (double)d->np;
-    if (d->dg_variant == PS_DG_UPF)
+    if (d->gen == PS_GEN_DG_TC)
+      io->bytes_shared = 0;
+    else if (d->dg_variant == PS_DG_UPF)
       io->bytes_shared = eb * ((double)u * (1.0 + (double)d->np));
     else if (d->dg_variant != PS_DG_NOPF)
       io->bytes_shared = eb * (double)d->nmat * (double)d->np * (double)d->np *
@@ -52,7 +54,7 @@ int dg_io(const ps_kernel_desc* d, ps_io_info* io) {
 }
 
 const char* dg_input_name(const ps_kernel_desc* d, int i) {
-  if (d->gen == PS_GEN_DG) return i == 0 ? "diff_mat" : "u";
+  if (d->gen == PS_GEN_DG || d->gen == PS_GEN_DG_TC) return i == 0 ? "diff_mat" : "u";
   return d->keep == PS_KEEP_U ? "u" : "diff_mat";
 }
 

@@ -1,0 +1,317 @@
+// K19: dg_diff_tc — DG differentiation as a dense contraction on the 5th-gen
+// tensor cores (an extra variant flagged as a dense contraction, not a paper
+// variant; BASELINE north_star "tcgen05 matmul/DG variant").
+//
+//   res[m, k, i] = sum_j dm[m, i, j] u[k, j]   i.e.   Res_m = U . Dm_m^T
+//
+// with U = u [nel][Np] (row-major, K = j contiguous: the MMA's A operand
+// K-major) and Dm_m = dm[m] [Np][Np] (rows i = N, K = j contiguous: the B
+// operand K-major), so neither operand needs a transpose. tcgen05.mma
+// kind::tf32, M = 128 element rows per tile, N = Np per matrix (nmat MMAs per
+// K step into adjacent TMEM column ranges), K = 8 per instruction.
+//
+// The contraction is tall and skinny (K = N = Np <= 128): 6 Np^2 flop per
+// 16 Np bytes of u in and res out, 0.375 Np flop/B — HBM-bound on tensor
+// cores at every order, so the design streams: the dm matrices are loaded
+// once per CTA and stay in shared memory; u tiles (128 rows x 32 columns,
+// 128-byte swizzle, zero-filled past nel and past Np) flow through a TMA
+// ring; accumulators double-buffer in TMEM when 2 nmat Np <= 512 columns so
+// the epilogue of one tile overlaps the loads and MMAs of the next.
+// Persistent CTAs (one per SM), 6 warps: 0 TMA, 1 MMA issue, 2-5 epilogue
+// (warp w drains TMEM lanes 32(w%4).. = element rows, 16-byte streaming
+// stores, rows >= nel masked).
+//
+// Parity: seed-pattern inputs are small integers, exact in TF32, with FP32
+// sums < 2^24 (Np <= 128: 128 * 17^2), so the result equals the fp32 oracle
+// bit for bit; on U[-1,1) inputs the TF32 operand rounding bounds the error
+// (tests/test_gpu_dg_tc.py).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "runtime_internal.h"
+
+namespace ps {
+namespace {
+
+constexpr int BM = 128, BK = 32;    // element rows per tile; fp32 per 128-byte row
+constexpr int U_BLK = BM * BK * 4;  // 16 KB per K block of a u tile
+constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in dynamic shared memory
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "DGTC_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra DGTC_WAIT;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+// K-major, 128-byte swizzle: 8-row groups 1024 B apart (SBO), LBO unused.
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t saddr) {
+  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(0u)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+template <int W>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&v)[W]);
+template <>
+__device__ __forceinline__ void tmem_ld<32>(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_ld<16>(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int W>
+__device__ __forceinline__ void drain(uint32_t taddr, float* dst, bool live) {
+  uint32_t v[W];
+  tmem_ld<W>(taddr, v);  // warp-collective: every lane, live row or not
+  if (live) {
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q)
+      __stcs(reinterpret_cast<float4*>(dst + 4 * q),
+             make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                         __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+  }
+}
+
+template <int NP>
+struct Cfg {
+  static constexpr int NKB = (NP + BK - 1) / BK;  // 32-wide K blocks
+  static constexpr int DM_BLK = NP * 128;         // one (m, K block) of dm: NP rows x 128 B
+  static constexpr int STAGES = NP >= 128 ? 2 : 4;
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NP >> 3) << 17) |
+                                    (uint32_t(BM >> 4) << 24);
+  static int smem_bytes(int nmat) { return nmat * NKB * DM_BLK + STAGES * U_BLK + 1024 + 256; }
+};
+
+template <int NP>
+__global__ void __launch_bounds__(192, 1)
+    dg_tc_kernel(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmD,
+                 float* __restrict__ res, int64_t nel, int nmat, int nacc, uint32_t tmem_cols) {
+  using C = Cfg<NP>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sdm = smem;                                  // [m][kb] blocks of NP x 128 B
+  uint8_t* su = smem + nmat * C::NKB * C::DM_BLK;       // STAGES x (128 x 128 B)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(su + C::STAGES * U_BLK);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 5);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (nel + BM - 1) / BM;
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + C::STAGES);
+  const uint32_t tfull0 = smem_u32(bars + 2 * C::STAGES), tempty0 = tfull0 + 16;
+  const uint32_t dm_full = tfull0 + 32;
+  const uint32_t acc_cols = uint32_t(nmat * NP);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull0 + 8 * a, 1);
+      mbar_init(tempty0 + 8 * a, 128);
+    }
+    mbar_init(dm_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA: dm once, then the u ring across this CTA's tiles
+      mbar_expect_tx(dm_full, uint32_t(nmat * C::NKB * C::DM_BLK));
+      for (int m = 0; m < nmat; ++m)
+        for (int kb = 0; kb < C::NKB; ++kb)
+          tma_2d(smem_u32(sdm + (m * C::NKB + kb) * C::DM_BLK), &tmD, dm_full, kb * BK, m * NP);
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int kb = 0; kb < C::NKB; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          if (it >= C::STAGES) mbar_wait(empty0 + 8 * s, ((it / C::STAGES) - 1) & 1);
+          mbar_expect_tx(full0 + 8 * s, U_BLK);
+          tma_2d(smem_u32(su + s * U_BLK), &tmU, full0 + 8 * s, kb * BK, int(t * BM));
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issue
+      mbar_wait(dm_full, 0);
+      int it = 0, local = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+        const int a = local % nacc;
+        const int use = local / nacc;  // how often accumulator a was used before
+        if (use >= 1) mbar_wait(tempty0 + 8 * a, (use - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d0 = tmem + uint32_t(a) * acc_cols;
+        for (int kb = 0; kb < C::NKB; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          mbar_wait(full0 + 8 * s, (it / C::STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t ub = smem_u32(su + s * U_BLK);
+          const int nks = (NP - kb * BK) >= BK ? BK / 8 : (NP - kb * BK) / 8;
+          for (int m = 0; m < nmat; ++m) {
+            const uint32_t db = smem_u32(sdm + (m * C::NKB + kb) * C::DM_BLK);
+            for (int ks = 0; ks < nks; ++ks)
+              mma_tf32(d0 + uint32_t(m * NP), desc_kmajor(ub + ks * 32), desc_kmajor(db + ks * 32), C::IDESC,
+                       (kb | ks) != 0);
+          }
+          mma_commit(empty0 + 8 * s);
+        }
+        mma_commit(tfull0 + 8 * a);
+      }
+    }
+  } else {  // epilogue: warp w <-> TMEM lanes 32(w%4).. = element rows
+    const int q4 = warp & 3;
+    int local = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+      const int a = local % nacc;
+      mbar_wait(tfull0 + 8 * a, (local / nacc) & 1);
+      __syncwarp();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t row = t * BM + 32 * q4 + lane;
+      const bool live = row < nel;
+      const uint32_t tb = tmem + (uint32_t(32 * q4) << 16) + uint32_t(a) * acc_cols;
+      for (int m = 0; m < nmat; ++m) {
+        float* dst = res + ((int64_t)m * nel + row) * NP;
+#pragma unroll
+        for (int c = 0; c + 32 <= NP; c += 32) drain<32>(tb + uint32_t(m * NP + c), dst + c, live);
+        if constexpr (NP % 32 == 16) drain<16>(tb + uint32_t(m * NP + NP - 16), dst + NP - 16, live);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty0 + 8 * a) : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols) : "memory");
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q{};
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D fp32 row-major [rows][cols], box 32 columns x box_rows, 128-byte swizzle,
+// out-of-range elements zero-filled.
+int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return set_error(PS_ERR_CUDA, "dg_diff_tc: cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(cols) * 4};
+  const cuuint32_t box[2] = {BK, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(PS_ERR_CUDA, "dg_diff_tc: cuTensorMapEncodeTiled failed (%d)", int(r));
+  return PS_OK;
+}
+
+template <int NP>
+int launch_np(Ctx* c, const ps_kernel_desc* d) {
+  using C = Cfg<NP>;
+  const int nmat = (int)d->nmat;
+  const int smem = C::smem_bytes(nmat);
+  if (smem > SMEM_LIMIT)
+    return set_error(PS_ERR_ARG, "dg_diff_tc: %d matrices of %d nodes exceed shared memory", nmat, NP);
+  static std::once_flag attr;
+  std::call_once(attr, [] {
+    cudaFuncSetAttribute(dg_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
+  });
+  const int cols = nmat * NP;
+  const int nacc = 2 * cols <= 512 ? 2 : 1;
+  uint32_t tcols = 32;
+  while (tcols < uint32_t(nacc * cols)) tcols <<= 1;
+  CUtensorMap tu, td;
+  int rc = make_map(&tu, c->in[1].ptr, d->nel, NP, BM);
+  if (rc) return rc;
+  rc = make_map(&td, c->in[0].ptr, (int64_t)nmat * NP, NP, NP);
+  if (rc) return rc;
+  const int64_t ntiles = (d->nel + BM - 1) / BM;
+  const int grid = (int)(ntiles < c->sm_count ? ntiles : c->sm_count);
+  dg_tc_kernel<NP><<<grid, 192, smem, c->stream>>>(tu, td, (float*)c->out[0].ptr, d->nel, nmat, nacc, tcols);
+  return PS_OK;
+}
+
+}  // namespace
+
+int dg_tc_launch(Ctx* c, const ps_kernel_desc* d) {
+  switch (d->np) {
+    case 16: return launch_np<16>(c, d);
+    case 32: return launch_np<32>(c, d);
+    case 48: return launch_np<48>(c, d);
+    case 64: return launch_np<64>(c, d);
+    case 80: return launch_np<80>(c, d);
+    case 96: return launch_np<96>(c, d);
+    case 112: return launch_np<112>(c, d);
+    case 128: return launch_np<128>(c, d);
+    default: return set_error(PS_ERR_ARG, "dg_diff_tc supports nunit_nodes 16..128 (multiples of 16)");
+  }
+}
+
+}  // namespace ps

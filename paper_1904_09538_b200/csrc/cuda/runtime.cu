@@ -163,6 +163,10 @@ int parse_variant_id(const char* id, ps_kernel_desc* d) {
         return set_error(PS_ERR_ARG, "variant '%s': keep must be u or res", id);
       d->keep = kt->second == "u" ? PS_KEEP_U : PS_KEEP_RES;
     }
+  } else if (gen == "dg_diff_tc") {
+    d->gen = PS_GEN_DG_TC;
+    ok = need_i("nelements", &d->nel) && need_i("nunit_nodes", &d->np) &&
+         need_i("nmatrices", &d->nmat);
   } else if (gen == "dg_diff" || gen == "dg_diff_rm") {
     d->gen = gen == "dg_diff" ? PS_GEN_DG : PS_GEN_DG_RM;
     ok = need_i("nelements", &d->nel) && need_i("nunit_nodes", &d->np) &&
@@ -244,6 +248,7 @@ int validate_desc(const ps_kernel_desc* d) {
     }
     case PS_GEN_DG:
     case PS_GEN_DG_RM:
+    case PS_GEN_DG_TC:
       return dg_validate(d);
     default:
       return set_error(PS_ERR_ARG, "unknown generator %d", d->gen);
@@ -331,6 +336,7 @@ int kernel_io(const ps_kernel_desc* d, ps_io_info* io) {
     }
     case PS_GEN_DG:
     case PS_GEN_DG_RM:
+    case PS_GEN_DG_TC:
       return dg_io(d, io);
     default:
       return set_error(PS_ERR_ARG, "unknown generator %d", d->gen);
@@ -349,7 +355,8 @@ static const char* input_name(const ps_kernel_desc* d, int i) {
     case PS_GEN_FD:
     case PS_GEN_FD_RM: return "u";
     case PS_GEN_DG:
-    case PS_GEN_DG_RM: return dg_input_name(d, i);
+    case PS_GEN_DG_RM:
+    case PS_GEN_DG_TC: return dg_input_name(d, i);
     default: return "x";
   }
 }
@@ -705,6 +712,8 @@ int launch(Ctx* c, const ps_kernel_desc* d) {
       return dg_launch(c, d);
     case PS_GEN_MATMUL_TC:
       return tc_launch(c, d);
+    case PS_GEN_DG_TC:
+      return dg_tc_launch(c, d);
     default:
       return set_error(PS_ERR_ARG, "unknown generator %d", d->gen);
   }

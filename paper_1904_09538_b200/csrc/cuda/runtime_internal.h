@@ -78,6 +78,7 @@ int dg_io(const ps_kernel_desc* d, ps_io_info* io);
 const char* dg_input_name(const ps_kernel_desc* d, int i);
 int dg_launch(Ctx* c, const ps_kernel_desc* d);
 int tc_launch(Ctx* c, const ps_kernel_desc* d);
+int dg_tc_launch(Ctx* c, const ps_kernel_desc* d);
 
 }  // namespace ps
 

@@ -16,6 +16,7 @@ INPUT_NAMES = {
     11: lambda d, i: "diff_mat" if i == 0 else "u",
     12: lambda d, i: "u" if d.keep == 3 else "diff_mat",
     13: lambda d, i: "a" if i == 0 else "b",
+    14: lambda d, i: "diff_mat" if i == 0 else "u",
 }
 
 

@@ -1,0 +1,65 @@
+"""K19 dg_diff_tc (DG as a tcgen05 kind::tf32 contraction, an extra dense-
+contraction variant) against the fp32 oracle. Seed-pattern inputs are small
+integers, exact in TF32, with FP32 sums < 2^24 (Np <= 128), so the result must
+equal the oracle bit for bit — including partial 128-row tiles (rows past nel
+masked, TMA zero fill) and Np that are not multiples of 32 (16, 48, zero-filled
+K columns). On U[-1,1) inputs: |res - exact| <= 2^-10 * (|dm| . |u|)
+elementwise (TF32 operand rounding, as for K16)."""
+import numpy as np
+import pytest
+
+from oracle import suite as oracle_suite
+from tests._inputs import desc_io, make_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _id(nel, np_, nmat=3):
+    return f"dg_diff_tc__dtype-float32__nelements-{nel}__nmatrices-{nmat}__nunit_nodes-{np_}"
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_1904_09538_b200.device import CudaDevice
+    d = CudaDevice(0)
+    yield d
+    d.close()
+
+
+@pytest.mark.parametrize("np_", [16, 32, 48, 64, 96, 128])
+@pytest.mark.parametrize("nel", [16, 1040, 40000])
+def test_dg_tc_seed_pattern_bitwise(dev, nel, np_):
+    d, io = desc_io(_id(nel, np_))
+    ins = make_inputs(d, io, "seed17")
+    got = dev.run(d, ins)[0]
+    want = oracle_suite.run(d, io, ins)[0]
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("nmat", [1, 2, 4])
+def test_dg_tc_other_matrix_counts(dev, nmat):
+    d, io = desc_io(_id(272, 64, nmat))
+    ins = make_inputs(d, io, "seed17")
+    np.testing.assert_array_equal(dev.run(d, ins)[0].view(np.uint32),
+                                  oracle_suite.run(d, io, ins)[0].view(np.uint32))
+
+
+@pytest.mark.parametrize("np_", [48, 128])
+def test_dg_tc_uniform_within_tf32_bound(dev, np_):
+    nel, nmat = 1040, 3
+    d, io = desc_io(_id(nel, np_))
+    ins = make_inputs(d, io, "uniform", seed=5)
+    got = dev.run(d, ins)[0].astype(np.float64).reshape(nmat, nel, np_)
+    dm = ins[0].astype(np.float64).reshape(nmat, np_, np_)
+    u = ins[1].astype(np.float64).reshape(nel, np_)
+    exact = np.einsum("mij,kj->mki", dm, u)
+    bound = 2.0 ** -10 * np.einsum("mij,kj->mki", np.abs(dm), np.abs(u))
+    assert np.all(np.abs(got - exact) <= bound)
+    assert np.max(np.abs(got - exact) / bound) > 1e-3  # a TF32 result, not FP32
+
+
+def test_dg_tc_rejects_shared_memory_overflow(dev):
+    from paper_1904_09538_b200 import PsError
+    d, io = desc_io(_id(256, 128, 4))
+    with pytest.raises(PsError, match="exceed shared memory"):
+        dev.run(d, make_inputs(d, io, "seed17"))
