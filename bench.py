@@ -463,6 +463,35 @@ def tensor_variant_report(dev, n: int = 8192, trials: int = 10) -> dict:
     return out
 
 
+def dg_tensor_variant_report(dev, mean_s: dict[str, float], nel: int = 1_000_000,
+                             trials: int = 10) -> dict:
+    """dg_diff_tc (K19: DG as a tcgen05 kind::tf32 contraction) at nel and every
+    order's padded Np, timed like every suite kernel, against its HBM roofline
+    (u in + res out + dm, MEASURED_PEAKS.json) and the fastest paper variant of
+    the same size from this run's sweep."""
+    from paper_1904_09538_b200 import desc_from_id, kernel_io
+    pk, src = peaks()
+    rows = {}
+    for np_ in (16, 32, 48, 64, 96, 128):
+        vid = f"dg_diff_tc__dtype-float32__nelements-{nel}__nmatrices-3__nunit_nodes-{np_}"
+        io = kernel_io(desc_from_id(vid))
+        dev.prepare(vid)
+        dev.measure(vid, trials=3, warmup=0)
+        mean, _ = dev.measure_summary(vid, trials=trials, warmup=2)
+        best = min(((t, k) for k, t in mean_s.items()
+                    if k.startswith("dg_diff__") and f"__nelements-{nel}__" in k
+                    and f"__nunit_nodes-{np_}__" in k), default=(None, None))
+        gbs = io.bytes_global / mean / 1e9
+        rows[str(np_)] = {"ms": round(mean * 1e3, 4), "GBps": round(gbs, 1),
+                          "hbm_frac": round(gbs / pk["hbm_gbs"], 4),
+                          "tflops": round(io.flops / mean / 1e12, 1),
+                          "best_paper_variant": best[1].rsplit("variant-", 1)[-1] if best[1] else None,
+                          "speedup_vs_best_paper_variant": round(best[0] / mean, 2) if best[0] else None}
+    return {"kernel": f"dg_diff_tc__dtype-float32__nelements-{nel}__nmatrices-3__nunit_nodes-*",
+            "bound": "hbm", "peak_GBps": pk["hbm_gbs"], "peak_source": src,
+            "dtype": "tf32 operands, fp32 accumulate", "by_nunit_nodes": rows}
+
+
 # ---------------------------------------------------------------------------
 # C5: the calibrated models evaluated over a large variant space (K18)
 
@@ -891,6 +920,8 @@ def run_ours(args, dist: Dist) -> None:
         diagnosis = {"error": str(e)}
     try:
         tensor_variant = tensor_variant_report(dev) if args.tc else None
+        if args.tc and tensor_variant is not None and any(w.name == "dg" for w, _, _ in parts):
+            tensor_variant["dg_diff_tc"] = dg_tensor_variant_report(dev, mean_s)
     except Exception as e:
         tensor_variant = {"error": str(e)}
     n_app = sum(len(app) for _, _, app in parts)
