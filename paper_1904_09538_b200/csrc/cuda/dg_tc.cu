@@ -31,6 +31,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "runtime_internal.h"
@@ -116,11 +117,10 @@ template <int NP>
 struct Cfg {
   static constexpr int NKB = (NP + BK - 1) / BK;  // 32-wide K blocks
   static constexpr int DM_BLK = NP * 128;         // one (m, K block) of dm: NP rows x 128 B
-  // shared memory (3 matrices): resident dm + u ring + epilogue buffers
-  // (4 warps x OUT_BUFS x 32 rows x 128 B) within 227 KB; at Np = 128 the dm
-  // matrices alone take 192 KB, leaving one u stage and one buffer per warp
-  static constexpr int STAGES = NP >= 128 ? 1 : NP >= 112 ? 2 : 4;
-  static constexpr int OUT_BUFS = NP >= 112 ? 1 : 2;
+  // shared memory: the CTA's resident dm matrices + a 4-stage u ring + two
+  // epilogue buffers per warp (4 x 2 x 32 rows x 128 B) within 227 KB
+  static constexpr int STAGES = 4;
+  static constexpr int OUT_BUFS = 2;
   static constexpr int OUT_BYTES = 4 * OUT_BUFS * 4096;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NP >> 3) << 17) |
                                     (uint32_t(BM >> 4) << 24);
@@ -130,8 +130,12 @@ struct Cfg {
 template <int NP>
 __global__ void __launch_bounds__(192, 1)
     dg_tc_kernel(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmD,
-                 const __grid_constant__ CUtensorMap tmR, int64_t nel, int nmat, int nacc,
+                 const __grid_constant__ CUtensorMap tmR, int64_t nel, int nmat, int groups, int nacc,
                  uint32_t tmem_cols) {
+  // CTA groups: when all matrices do not fit beside the u ring (Np >= 112),
+  // group g of the grid owns matrices [g*nmat, (g+1)*nmat) (nmat per CTA) and
+  // every group walks all tiles in the same order, so the groups read each
+  // u tile close together in time and all but the first read hit in L2
   using C = Cfg<NP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
@@ -143,6 +147,8 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 5);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (nel + BM - 1) / BM;
+  const int grp = blockIdx.x % groups, cta = blockIdx.x / groups, ncta = gridDim.x / groups;
+  const int m0 = grp * nmat;
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + C::STAGES);
   const uint32_t tfull0 = smem_u32(bars + 2 * C::STAGES), tempty0 = tfull0 + 16;
   const uint32_t dm_full = tfull0 + 32;
@@ -176,9 +182,9 @@ __global__ void __launch_bounds__(192, 1)
       mbar_expect_tx(dm_full, uint32_t(nmat * C::NKB * C::DM_BLK));
       for (int m = 0; m < nmat; ++m)
         for (int kb = 0; kb < C::NKB; ++kb)
-          tma_2d(smem_u32(sdm + (m * C::NKB + kb) * C::DM_BLK), &tmD, dm_full, kb * BK, m * NP);
+          tma_2d(smem_u32(sdm + (m * C::NKB + kb) * C::DM_BLK), &tmD, dm_full, kb * BK, (m0 + m) * NP);
       int it = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int64_t t = cta; t < ntiles; t += ncta)
         for (int kb = 0; kb < C::NKB; ++kb, ++it) {
           const int s = it % C::STAGES;
           if (it >= C::STAGES) mbar_wait(empty0 + 8 * s, ((it / C::STAGES) - 1) & 1);
@@ -190,7 +196,7 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {  // MMA issue
       mbar_wait(dm_full, 0);
       int it = 0, local = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+      for (int64_t t = cta; t < ntiles; t += ncta, ++local) {
         const int a = local % nacc;
         const int use = local / nacc;  // how often accumulator a was used before
         if (use >= 1) mbar_wait(tempty0 + 8 * a, (use - 1) & 1);
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(192, 1)
   } else {  // epilogue: warp w <-> TMEM lanes 32(w%4).. = element rows
     const int q4 = warp & 3;
     int local = 0, nchunk = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+    for (int64_t t = cta; t < ntiles; t += ncta, ++local) {
       const int a = local % nacc;
       mbar_wait(tfull0 + 8 * a, (local / nacc) & 1);
       __syncwarp();
@@ -259,7 +265,7 @@ __global__ void __launch_bounds__(192, 1)
             asm volatile(
                 "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                     reinterpret_cast<uint64_t>(&tmR)),
-                "r"(c), "r"(int(t * BM + 32 * q4)), "r"(m), "r"(ob)
+                "r"(c), "r"(int(t * BM + 32 * q4)), "r"(m0 + m), "r"(ob)
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
@@ -321,10 +327,13 @@ int make_res_map(CUtensorMap* m, void* base, int64_t nel, int64_t np, int64_t nm
 template <int NP>
 int launch_np(Ctx* c, const ps_kernel_desc* d) {
   using C = Cfg<NP>;
-  const int nmat = (int)d->nmat;
+  const int nmat_all = (int)d->nmat;
+  // all matrices per CTA when they fit, else one matrix per CTA (nmat groups)
+  const int groups = C::smem_bytes(nmat_all) <= SMEM_LIMIT ? 1 : nmat_all;
+  const int nmat = nmat_all / groups;
   const int smem = C::smem_bytes(nmat);
   if (smem > SMEM_LIMIT)
-    return set_error(PS_ERR_ARG, "dg_diff_tc: %d matrices of %d nodes exceed shared memory", nmat, NP);
+    return set_error(PS_ERR_ARG, "dg_diff_tc: %d nodes per element exceed shared memory", NP);
   static std::once_flag attr;
   std::call_once(attr, [] {
     cudaFuncSetAttribute(dg_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
@@ -336,14 +345,15 @@ int launch_np(Ctx* c, const ps_kernel_desc* d) {
   CUtensorMap tu, td;
   int rc = make_map(&tu, c->in[1].ptr, d->nel, NP, BM);
   if (rc) return rc;
-  rc = make_map(&td, c->in[0].ptr, (int64_t)nmat * NP, NP, NP);
+  rc = make_map(&td, c->in[0].ptr, (int64_t)nmat_all * NP, NP, NP);
   if (rc) return rc;
   CUtensorMap tr;
-  rc = make_res_map(&tr, c->out[0].ptr, d->nel, NP, nmat);
+  rc = make_res_map(&tr, c->out[0].ptr, d->nel, NP, nmat_all);
   if (rc) return rc;
   const int64_t ntiles = (d->nel + BM - 1) / BM;
-  const int grid = (int)(ntiles < c->sm_count ? ntiles : c->sm_count);
-  dg_tc_kernel<NP><<<grid, 192, smem, c->stream>>>(tu, td, tr, d->nel, nmat, nacc, tcols);
+  const int64_t per_group = std::min<int64_t>(ntiles, std::max(1, c->sm_count / groups));
+  const int grid = (int)(per_group * groups);
+  dg_tc_kernel<NP><<<grid, 192, smem, c->stream>>>(tu, td, tr, d->nel, nmat, groups, nacc, tcols);
   return PS_OK;
 }
 
