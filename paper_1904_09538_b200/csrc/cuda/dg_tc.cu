@@ -117,10 +117,11 @@ template <int NP>
 struct Cfg {
   static constexpr int NKB = (NP + BK - 1) / BK;  // 32-wide K blocks
   static constexpr int DM_BLK = NP * 128;         // one (m, K block) of dm: NP rows x 128 B
-  // shared memory: the CTA's resident dm matrices + a 4-stage u ring + two
-  // epilogue buffers per warp (4 x 2 x 32 rows x 128 B) within 227 KB
-  static constexpr int STAGES = 4;
-  static constexpr int OUT_BUFS = 2;
+  // shared memory: the CTA's resident dm matrices + a u ring (8 stages at
+  // Np <= 32, whose tiles are short, else 4) + epilogue buffers per warp
+  // (4 warps x OUT_BUFS x 32 rows x 128 B) within 227 KB
+  static constexpr int STAGES = NP <= 32 ? 8 : 4;
+  static constexpr int OUT_BUFS = NP <= 32 ? 4 : 2;
   static constexpr int OUT_BYTES = 4 * OUT_BUFS * 4096;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NP >> 3) << 17) |
                                     (uint32_t(BM >> 4) << 24);
@@ -238,7 +239,9 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t ob = ob0 + uint32_t(nchunk % C::OUT_BUFS) * 4096;
           if (nchunk >= C::OUT_BUFS) {  // the store that last read this buffer is done
             if (lane == 0) {
-              if constexpr (C::OUT_BUFS == 2)
+              if constexpr (C::OUT_BUFS == 4)
+                asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+              else if constexpr (C::OUT_BUFS == 2)
                 asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
               else
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
