@@ -158,6 +158,13 @@ __device__ __forceinline__ void tile_coords(int t, int mt, int& m0, int& n0) {
   n0 = (band * TILE_BAND + r / mt) * BN;
 }
 
+__device__ __forceinline__ void tile_coords2(int t, int mt, int& m0, int& n0) {
+  const int per_band = TILE_BAND * mt;
+  const int band = t / per_band, r = t - band * per_band;
+  m0 = (r % mt) * 256;
+  n0 = (band * TILE_BAND + r / mt) * BN;
+}
+
 // BMN: B is loaded N-major straight from row-major B[k][n] — one 3-D TMA box
 // of 8 N-atoms x 32 k-rows x 32 n (128 B rows, 128B swizzle with 32-byte
 // atomicity, the only MN-major layout tf32 accepts), atoms 4 KB apart (LBO),
@@ -290,6 +297,179 @@ __global__ void __launch_bounds__(192, 1)
                  : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair version (cta_group::2): a cluster of 2 CTAs on one TPC computes a
+// 256 x 256 tile with M = 256 MMAs issued by the leader (rank 0). Each CTA
+// stages its own 128 rows of A and its own 128-column half of B (N-major)
+// per 32-deep K block, so a pair reads 2 x (128 + 128) x 32 operands per K
+// block for a 256 x 256 tile instead of 2 x (128 + 256) x 32 for two 128 x 256
+// tiles: a third less L2 -> SM traffic. Both CTAs' TMA loads complete on the
+// leader's stage barrier (.cta_group::2, peer bit cleared); the leader's
+// tcgen05.commit multicasts stage-free / accumulator-ready to both CTAs; both
+// epilogues drain their own TMEM rows and arrive on the leader's
+// accumulator-free barrier through its cluster address.
+constexpr int BM2 = 256, STAGES2 = 6;
+constexpr int A2_BYTES = 128 * BK * 4;        // this CTA's 128 rows of A
+constexpr int B2_BYTES = (BN / 2) * BK * 4;   // this CTA's 128 columns of B
+constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
+constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 1024 + 256;
+constexpr uint32_t IDESC2 = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | (uint32_t(BN >> 3) << 17) |
+                            (uint32_t(BM2 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t leader_addr(uint32_t local) {  // same offset in cluster rank 0
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(local));
+  return r;
+}
+__device__ __forceinline__ void tma2_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(IDESC2), "r"(acc), "r"(0u)
+      : "memory");
+}
+__device__ __forceinline__ void commit2(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((unsigned short)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    matmul_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      float* __restrict__ C, int n) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;                            // STAGES2 x (128 x 32) A
+  uint8_t* sb = smem + STAGES2 * A2_BYTES;       // STAGES2 x (32 x 128) B half, N-major
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + STAGES2 * B2_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES2 + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int nk = n / BK;
+  const int mt = n / BM2, ntiles = mt * (n / BN);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES2);
+  const uint32_t tfull0 = smem_u32(bars + 2 * STAGES2), tempty0 = smem_u32(bars + 2 * STAGES2 + 2);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull0 + 8 * a, 1);
+      mbar_init(tempty0 + 8 * a, 256);  // both CTAs' epilogue threads (leader's copy)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs): own A rows and own B half
+      int it = 0;
+      for (int t = pair; t < ntiles; t += npairs) {
+        int m0, n0;
+        tile_coords2(t, mt, m0, n0);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES2;
+          if (it >= STAGES2) mbar_wait(empty0 + 8 * s, ((it / STAGES2) - 1) & 1);
+          const uint32_t fb = full0 + 8 * s;
+          if (leader) mbar_expect_tx(fb, 2 * STAGE2_BYTES);
+          tma2_2d(smem_u32(sa + s * A2_BYTES), &tmA, fb, kb * BK, m0 + 128 * int(rank));
+          tma2_3d(smem_u32(sb + s * B2_BYTES), &tmB, fb, 0, kb * BK, (n0 + 128 * int(rank)) / 32);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // MMA issuer for the pair
+      int it = 0, local = 0;
+      for (int t = pair; t < ntiles; t += npairs, ++local) {
+        const int acc = local & 1;
+        const uint32_t d = tmem + uint32_t(acc * TMEM_COLS);
+        if (local >= 2) mbar_wait(tempty0 + 8 * acc, ((local >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES2;
+          mbar_wait(full0 + 8 * s, (it / STAGES2) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a_base = smem_u32(sa + s * A2_BYTES), b_base = smem_u32(sb + s * B2_BYTES);
+#pragma unroll
+          for (int ks = 0; ks < BK / UMMA_K; ++ks)
+            mma2_tf32(d, desc_sw128(a_base + ks * UMMA_K * 4, 16, 1024), desc_sw128_32b(b_base + ks * 1024, 4096, 512),
+                      (kb | ks) != 0);
+          commit2(empty0 + 8 * s);
+        }
+        commit2(tfull0 + 8 * acc);
+      }
+    }
+  } else {  // epilogue (both CTAs): this CTA's 128 rows of the 256 x 256 tile
+    const int q4 = warp & 3;
+    int local = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++local) {
+      int m0, n0;
+      tile_coords2(t, mt, m0, n0);
+      const int acc = local & 1;
+      mbar_wait(tfull0 + 8 * acc, (local >> 1) & 1);
+      __syncwarp();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = m0 + 128 * int(rank) + 32 * q4 + lane;
+      float* crow = C + (int64_t)row * n + n0;
+      const uint32_t tbase = tmem + (uint32_t(32 * q4) << 16) + uint32_t(acc * TMEM_COLS);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tbase + uint32_t(32 * c), v);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          __stcs(reinterpret_cast<float4*>(crow + 32 * c + 4 * q),
+                 make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                             __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader_addr(tempty0 + 8 * acc))
+                   : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TMEM_COLS) : "memory");
+}
+
 // Bt[j][i] = B[i][j], 32x32 tiles through shared memory (coalesced both ways).
 __global__ void __launch_bounds__(256) transpose_f32(const float* __restrict__ b,
                                                      float* __restrict__ bt, int n) {
@@ -350,6 +530,28 @@ int make_map_bmn(CUtensorMap* m, const void* base, int64_t n) {
   return PS_OK;
 }
 
+// B half for the CTA pair: box 32 n x 32 k x 4 atoms (128 columns)
+int make_map_bmn_half(CUtensorMap* m, const void* base, int64_t n) {
+  auto fn = encode_fn();
+  if (!fn) return set_error(PS_ERR_CUDA, "matmul_sq_tc: cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {32, cuuint64_t(n), cuuint64_t(n / 32)};
+  const cuuint64_t strides[2] = {cuuint64_t(n) * 4, 128};
+  const cuuint32_t box[3] = {32, BK, (BN / 2) / 32};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(PS_ERR_CUDA, "matmul_sq_tc: B half map failed (%d)", int(r));
+  return PS_OK;
+}
+
+int tc_mode() {  // 2 = CTA pairs (default), 1 = single CTA, 0 = transpose path
+  const char* e = std::getenv("PS_TC_B");
+  if (e && std::string(e) == "k") return 0;
+  const char* p = std::getenv("PS_TC_PAIR");
+  return (p && std::string(p) == "0") ? 1 : 2;
+}
+
 bool b_n_major() {
   const char* e = std::getenv("PS_TC_B");
   return !(e && std::string(e) == "k");
@@ -365,7 +567,19 @@ int tc_launch(Ctx* c, const ps_kernel_desc* d) {
   std::call_once(attr, [] {
     cudaFuncSetAttribute(matmul_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     cudaFuncSetAttribute(matmul_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(matmul_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
   });
+  if (tc_mode() == 2) {
+    CUtensorMap ta2, tb2;
+    int rc2 = make_map(&ta2, c->in[0].ptr, n, n, BK, 128);  // A: box 32 (k) x 128 (m)
+    if (rc2) return rc2;
+    rc2 = make_map_bmn_half(&tb2, c->in[1].ptr, n);
+    if (rc2) return rc2;
+    const int ntiles2 = (n / BM2) * (n / BN);
+    const int pairs = ntiles2 < c->sm_count / 2 ? ntiles2 : c->sm_count / 2;
+    matmul_tc2_kernel<<<2 * pairs, 192, SMEM2_BYTES, c->stream>>>(ta2, tb2, (float*)c->out[0].ptr, n);
+    return PS_OK;
+  }
   const int ntiles = (n / BM) * (n / BN);
   const int grid = ntiles < c->sm_count ? ntiles : c->sm_count;
   CUtensorMap ta, tb;
