@@ -408,15 +408,28 @@ uint64_t fnv1a_name(const char* name) {
 // ---------------------------------------------------------------------------
 // Context.
 
-int Ctx::ensure(DevBuf& b, size_t bytes) {
+// Device allocation; when HBM runs out (the resident-variant cache, other
+// processes on the GPU, fragmentation) the least-recently-used cached variants
+// other than `keep` are released and the allocation retried, and the cache
+// budget shrinks to what actually fitted.
+int Ctx::ensure(DevBuf& b, size_t bytes, const std::string* keep) {
   if (b.cap >= bytes && b.ptr) return PS_OK;
   if (b.ptr) cudaFree(b.ptr);
   b.ptr = nullptr;
   b.cap = 0;
-  cudaError_t e = cudaMalloc(&b.ptr, std::max<size_t>(bytes, 256));
-  if (e != cudaSuccess) {
+  for (;;) {
+    cudaError_t e = cudaMalloc(&b.ptr, std::max<size_t>(bytes, 256));
+    if (e == cudaSuccess) break;
     cudaGetLastError();
-    return set_error(PS_ERR_NOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    auto lru = slots.end();
+    for (auto it = slots.begin(); it != slots.end(); ++it)
+      if ((!keep || it->first != *keep) && (lru == slots.end() || it->second.last_use < lru->second.last_use))
+        lru = it;
+    if (lru == slots.end())
+      return set_error(PS_ERR_NOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    release(lru->second);
+    slots.erase(lru);
+    cache_cap = std::min(cache_cap, cache_bytes);
   }
   b.cap = std::max<size_t>(bytes, 256);
   return PS_OK;
@@ -479,7 +492,7 @@ int prepare(Ctx* c, const ps_kernel_desc* d, int fill_mode, uint64_t seed) {
   c->cache_bytes += need;
   for (int i = 0; i < io.n_inputs; ++i) {
     size_t bytes = (size_t)io.input_elems[i] * io.elem_bytes;
-    if ((rc = c->ensure(s.in[i], bytes))) return rc;
+    if ((rc = c->ensure(s.in[i], bytes, &key))) return rc;
     uint64_t h = fnv1a_name(input_name(d, i));
     int blocks = (int)std::min<int64_t>((io.input_elems[i] + 255) / 256, c->sm_count * 32);
     if (fill_mode == PS_FILL_SEED17)
@@ -491,7 +504,7 @@ int prepare(Ctx* c, const ps_kernel_desc* d, int fill_mode, uint64_t seed) {
   }
   for (int i = 0; i < io.n_outputs; ++i) {
     size_t bytes = (size_t)io.output_elems[i] * io.elem_bytes;
-    if ((rc = c->ensure(s.out[i], bytes))) return rc;
+    if ((rc = c->ensure(s.out[i], bytes, &key))) return rc;
     PS_CUDA(cudaMemsetAsync(s.out[i].ptr, 0, bytes, c->stream));
   }
   PS_CUDA(cudaStreamSynchronize(c->stream));
@@ -780,7 +793,10 @@ int ps_init(int device, ps_ctx** out) {
   {
     size_t fr = 0, tot = 0;
     PS_CUDA(cudaMemGetInfo(&fr, &tot));
-    c->cache_cap = (size_t)((double)fr * 0.7);  // resident-variant budget (HBM)
+    // resident-variant budget: all of HBM but 8 GB of headroom (the B200 sweep
+    // keeps ~160 GB of inputs and outputs resident; allocations that still
+    // fail evict least-recently-used variants, Ctx::ensure)
+    c->cache_cap = fr > (size_t)16e9 ? fr - (size_t)8e9 : (size_t)((double)fr * 0.5);
     if (const char* cap = getenv("PS_CACHE_GB")) c->cache_cap = (size_t)(atof(cap) * 1e9);
   }
   const char* gen = getenv("PS_GMEM_GENERIC");

@@ -61,7 +61,7 @@ struct Ctx {
   float flop_base = 0.5f;
   float flop_step = 0.015625f;
 
-  int ensure(DevBuf& b, size_t bytes);
+  int ensure(DevBuf& b, size_t bytes, const std::string* keep = nullptr);
   void activate(Slot& s);
   void release(Slot& s);
 };
