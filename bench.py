@@ -816,6 +816,9 @@ def run_ours(args, dist: Dist) -> None:
     for ins, outs in pinned.values():
         for a in ins + outs:
             a.free()
+    # the sweep's resident arrays are no longer needed: give the fits, the
+    # prediction tables and the variant reports their HBM back
+    dev.trim()
 
     # ----- measurement table -> summaries (every rank holds the gathered table) -----
     trials: dict[int, list[float]] = {}

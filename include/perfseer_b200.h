@@ -169,6 +169,9 @@ int ps_run_host(ps_ctx* ctx, const ps_kernel_desc* desc, const void* const* inpu
  * (New; the batched form of ps_run_host for sweeps through host data.) */
 int ps_run_host_batch(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const void* const* inputs,
                       void* const* outputs, double* seconds);
+/* Releases every resident prepared variant and staging buffer of the context
+ * (the context, its stream and events stay valid; later calls re-prepare). */
+int ps_trim(ps_ctx* ctx);
 /* Pinned host memory for ps_run_host callers. */
 int ps_host_alloc(size_t bytes, void** ptr);
 int ps_host_free(void* ptr);

@@ -1108,6 +1108,21 @@ int ps_run_host_batch(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const voi
   return PS_OK;
 }
 
+int ps_trim(ps_ctx* ctx) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_error(PS_ERR_ARG, "ps_trim: null ctx");
+  PS_CUDA(cudaSetDevice(c->device));
+  PS_CUDA(cudaStreamSynchronize(c->stream));
+  for (auto& kv : c->slots) c->release(kv.second);
+  c->slots.clear();
+  c->cache_bytes = 0;
+  c->release(c->host_slot);
+  c->release(c->pipe_slot[0]);
+  c->release(c->pipe_slot[1]);
+  c->prepared = false;
+  return PS_OK;
+}
+
 int ps_host_alloc(size_t bytes, void** ptr) {
   if (!ptr) return set_error(PS_ERR_ARG, "ps_host_alloc: null out");
   PS_CUDA(cudaHostAlloc(ptr, bytes, cudaHostAllocDefault));

@@ -117,6 +117,10 @@ class CudaDevice:
         return s.value
 
 
+    def trim(self) -> None:
+        """Release every resident variant and staging buffer (ps_trim)."""
+        check(lib().ps_trim(self._ctx))
+
     def run_host_batch(self, kernels, inputs: list[list["PinnedArray"]],
                        outputs: list[list["PinnedArray"]]) -> float:
         """A sweep through host data, pipelined (ps_run_host_batch): H2D of the
