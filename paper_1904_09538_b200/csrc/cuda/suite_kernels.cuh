@@ -470,23 +470,28 @@ __global__ void __launch_bounds__(FD_STRIP_THREADS) finite_diff_strip(const floa
   const int gcount = min(R, groups - R * (int)blockIdx.x);  // work-groups in this strip
   const int64_t W = n + 2;
   if constexpr (MODE != 2) {
+    // 8-byte loads and shared stores: n is a multiple of I (even), so the row
+    // pitch n + 2, the strip origin I*R*bx and the strip width I*gcount + 2
+    // are all even and every float2 is aligned and wholly inside or outside
+    constexpr int CJ2 = (SW + 63) / 64;  // 64-column chunks per strip row
     const int width = I * gcount + 2;
-    const float* base = u + (int64_t)(I * i_out) * W + col0 + lane;
-    float v[RW][CJ];
+    const float2* base = reinterpret_cast<const float2*>(u + (int64_t)(I * i_out) * W + col0) + lane;
+    float2 v[RW][CJ2];
 #pragma unroll
     for (int k = 0; k < RW; ++k) {
       const int r = warp + k * NW;
-      const float* row = base + (int64_t)r * W;
+      const float2* row = base + (int64_t)r * (W / 2);
 #pragma unroll
-      for (int j = 0; j < CJ; ++j)
-        v[k][j] = (r < T && lane + 32 * j < width) ? __ldg(row + 32 * j) : 0.0f;
+      for (int j = 0; j < CJ2; ++j)
+        v[k][j] = (r < T && 2 * (lane + 32 * j) < width) ? __ldg(row + 32 * j) : make_float2(0.0f, 0.0f);
     }
 #pragma unroll
     for (int k = 0; k < RW; ++k) {
       const int r = warp + k * NW;
       if (r < T) {
 #pragma unroll
-        for (int j = 0; j < CJ; ++j) reg[r][lane + 32 * j] = v[k][j];
+        for (int j = 0; j < CJ2; ++j)
+          if (2 * (lane + 32 * j) < P) *reinterpret_cast<float2*>(&reg[r][2 * (lane + 32 * j)]) = v[k][j];
       }
     }
     bar_sync();  // the R work-groups' fetch barriers, executed as one
