@@ -32,6 +32,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "runtime_internal.h"
@@ -85,6 +86,44 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
 }
+// CTA-pair helpers (cta_group::2): cluster rank, cluster barrier, the
+// leader's copy of a shared address, TMA completing on the leader's barrier
+// (peer bit cleared), leader-issued M = 256 MMA, multicast commit.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t leader_addr(uint32_t local) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(local));
+  return r;
+}
+__device__ __forceinline__ void tma2_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(0u)
+      : "memory");
+}
+__device__ __forceinline__ void commit2(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((unsigned short)3)
+      : "memory");
+}
+
 template <int W>
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&v)[W]);
 template <>
@@ -113,10 +152,12 @@ __device__ __forceinline__ void tmem_ld<16>(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int NP>
+template <int NP, bool PAIR = false>
 struct Cfg {
   static constexpr int NKB = (NP + BK - 1) / BK;  // 32-wide K blocks
-  static constexpr int DM_BLK = NP * 128;         // one (m, K block) of dm: NP rows x 128 B
+  // one (m, K block) of dm: NP rows x 128 B (a CTA pair: NP / 2 rows each)
+  static constexpr int DM_ROWS = PAIR ? NP / 2 : NP;
+  static constexpr int DM_BLK = DM_ROWS * 128;
   // shared memory: the CTA's resident dm matrices + a u ring (8 stages at
   // Np <= 32, whose tiles are short, else 4) + epilogue buffers per warp
   // (4 warps x OUT_BUFS x 32 rows x 128 B) within 227 KB
@@ -124,11 +165,15 @@ struct Cfg {
   static constexpr int OUT_BUFS = NP <= 32 ? 4 : 2;
   static constexpr int OUT_BYTES = 4 * OUT_BUFS * 4096;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NP >> 3) << 17) |
-                                    (uint32_t(BM >> 4) << 24);
+                                    (uint32_t((PAIR ? 2 * BM : BM) >> 4) << 24);
   static int smem_bytes(int nmat) { return nmat * NKB * DM_BLK + STAGES * U_BLK + OUT_BYTES + 1024 + 256; }
 };
 
-template <int NP>
+// PAIR: a cluster of two CTAs (cta_group::2) computes 256-row tiles with
+// M = 256 MMAs issued by the leader; each CTA holds its 128 rows of u and
+// the N-half (Np/2 rows) of every dm matrix, so at Np = 128 all three
+// matrices fit beside the u ring without the per-matrix groups.
+template <int NP, bool PAIR>
 __global__ void __launch_bounds__(192, 1)
     dg_tc_kernel(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmD,
                  const __grid_constant__ CUtensorMap tmR, int64_t nel, int nmat, int groups, int nacc,
@@ -137,7 +182,7 @@ __global__ void __launch_bounds__(192, 1)
   // group g of the grid owns matrices [g*nmat, (g+1)*nmat) (nmat per CTA) and
   // every group walks all tiles in the same order, so the groups read each
   // u tile close together in time and all but the first read hit in L2
-  using C = Cfg<NP>;
+  using C = Cfg<NP, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -147,8 +192,13 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sout + C::OUT_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 5);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t ntiles = (nel + BM - 1) / BM;
-  const int grp = blockIdx.x % groups, cta = blockIdx.x / groups, ncta = gridDim.x / groups;
+  constexpr int TROWS = PAIR ? 2 * BM : BM;  // element rows per tile (per pair)
+  const int64_t ntiles = (nel + TROWS - 1) / TROWS;
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  const int unit = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);  // CTA, or pair
+  const int units = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
+  const int grp = unit % groups, cta = unit / groups, ncta = units / groups;
   const int m0 = grp * nmat;
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + C::STAGES);
   const uint32_t tfull0 = smem_u32(bars + 2 * C::STAGES), tempty0 = tfull0 + 16;
@@ -162,39 +212,62 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
-      mbar_init(tempty0 + 8 * a, 128);
+      mbar_init(tempty0 + 8 * a, PAIR ? 256 : 128);  // pair: both CTAs' epilogues
     }
     mbar_init(dm_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(tmem_cols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync_all();
+  else
+    __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {  // TMA: dm once, then the u ring across this CTA's tiles
-      mbar_expect_tx(dm_full, uint32_t(nmat * C::NKB * C::DM_BLK));
+      const uint32_t dm_bytes = uint32_t(nmat * C::NKB * C::DM_BLK);
+      if (leader) mbar_expect_tx(dm_full, PAIR ? 2 * dm_bytes : dm_bytes);
       for (int m = 0; m < nmat; ++m)
-        for (int kb = 0; kb < C::NKB; ++kb)
-          tma_2d(smem_u32(sdm + (m * C::NKB + kb) * C::DM_BLK), &tmD, dm_full, kb * BK, (m0 + m) * NP);
+        for (int kb = 0; kb < C::NKB; ++kb) {
+          const uint32_t dst = smem_u32(sdm + (m * C::NKB + kb) * C::DM_BLK);
+          const int row = (m0 + m) * NP + int(rank) * C::DM_ROWS;
+          if constexpr (PAIR)
+            tma2_2d(dst, &tmD, dm_full, kb * BK, row);
+          else
+            tma_2d(dst, &tmD, dm_full, kb * BK, row);
+        }
       int it = 0;
       for (int64_t t = cta; t < ntiles; t += ncta)
         for (int kb = 0; kb < C::NKB; ++kb, ++it) {
           const int s = it % C::STAGES;
           if (it >= C::STAGES) mbar_wait(empty0 + 8 * s, ((it / C::STAGES) - 1) & 1);
-          mbar_expect_tx(full0 + 8 * s, U_BLK);
-          tma_2d(smem_u32(su + s * U_BLK), &tmU, full0 + 8 * s, kb * BK, int(t * BM));
+          const int row = int(t * TROWS) + int(rank) * BM;
+          if constexpr (PAIR) {
+            if (leader) mbar_expect_tx(full0 + 8 * s, 2 * U_BLK);
+            tma2_2d(smem_u32(su + s * U_BLK), &tmU, full0 + 8 * s, kb * BK, row);
+          } else {
+            mbar_expect_tx(full0 + 8 * s, U_BLK);
+            tma_2d(smem_u32(su + s * U_BLK), &tmU, full0 + 8 * s, kb * BK, row);
+          }
         }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issue
+    if (lane == 0 && leader) {  // MMA issue (a pair: the leader, for both CTAs)
       mbar_wait(dm_full, 0);
       int it = 0, local = 0;
       for (int64_t t = cta; t < ntiles; t += ncta, ++local) {
@@ -211,13 +284,18 @@ __global__ void __launch_bounds__(192, 1)
           const int nks = (NP - kb * BK) >= BK ? BK / 8 : (NP - kb * BK) / 8;
           for (int m = 0; m < nmat; ++m) {
             const uint32_t db = smem_u32(sdm + (m * C::NKB + kb) * C::DM_BLK);
-            for (int ks = 0; ks < nks; ++ks)
-              mma_tf32(d0 + uint32_t(m * NP), desc_kmajor(ub + ks * 32), desc_kmajor(db + ks * 32), C::IDESC,
-                       (kb | ks) != 0);
+            for (int ks = 0; ks < nks; ++ks) {
+              if constexpr (PAIR)
+                mma2_tf32(d0 + uint32_t(m * NP), desc_kmajor(ub + ks * 32), desc_kmajor(db + ks * 32), C::IDESC,
+                          (kb | ks) != 0);
+              else
+                mma_tf32(d0 + uint32_t(m * NP), desc_kmajor(ub + ks * 32), desc_kmajor(db + ks * 32), C::IDESC,
+                         (kb | ks) != 0);
+            }
           }
-          mma_commit(empty0 + 8 * s);
+          if constexpr (PAIR) commit2(empty0 + 8 * s); else mma_commit(empty0 + 8 * s);
         }
-        mma_commit(tfull0 + 8 * a);
+        if constexpr (PAIR) commit2(tfull0 + 8 * a); else mma_commit(tfull0 + 8 * a);
       }
     }
   } else {  // epilogue: warp w <-> TMEM lanes 32(w%4).. = element rows
@@ -268,20 +346,30 @@ __global__ void __launch_bounds__(192, 1)
             asm volatile(
                 "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                     reinterpret_cast<uint64_t>(&tmR)),
-                "r"(c), "r"(int(t * BM + 32 * q4)), "r"(m0 + m), "r"(ob)
+                "r"(c), "r"(int(t * TROWS) + int(rank) * BM + 32 * q4), "r"(m0 + m), "r"(ob)
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty0 + 8 * a) : "memory");
+      if constexpr (PAIR)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader_addr(tempty0 + 8 * a))
+                     : "memory");
+      else
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty0 + 8 * a) : "memory");
     }
   }
   if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols) : "memory");
+  if constexpr (PAIR) {
+    cluster_sync_all();
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols) : "memory");
+  } else {
+    __syncthreads();
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols) : "memory");
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -327,9 +415,17 @@ int make_res_map(CUtensorMap* m, void* base, int64_t nel, int64_t np, int64_t nm
   return PS_OK;
 }
 
-template <int NP>
-int launch_np(Ctx* c, const ps_kernel_desc* d) {
-  using C = Cfg<NP>;
+// CTA pairs for Np >= 112 on request (PS_DGTC_PAIR=1): correct (the same
+// parity tests pass in both modes) but measured no faster than the per-matrix
+// CTA groups (Np = 128: 5.31 vs 5.45 TB/s) — the groups' extra u reads hit L2.
+bool dg_pair_enabled() {
+  const char* e = std::getenv("PS_DGTC_PAIR");
+  return e && e[0] == '1';
+}
+
+template <int NP, bool PAIR>
+int launch_cfg(Ctx* c, const ps_kernel_desc* d) {
+  using C = Cfg<NP, PAIR>;
   const int nmat_all = (int)d->nmat;
   // all matrices per CTA when they fit, else one matrix per CTA (nmat groups)
   const int groups = C::smem_bytes(nmat_all) <= SMEM_LIMIT ? 1 : nmat_all;
@@ -339,25 +435,49 @@ int launch_np(Ctx* c, const ps_kernel_desc* d) {
     return set_error(PS_ERR_ARG, "dg_diff_tc: %d nodes per element exceed shared memory", NP);
   static std::once_flag attr;
   std::call_once(attr, [] {
-    cudaFuncSetAttribute(dg_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
+    cudaFuncSetAttribute(dg_tc_kernel<NP, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
   });
   const int cols = nmat * NP;
   const int nacc = 2 * cols <= 512 ? 2 : 1;
   uint32_t tcols = 32;
   while (tcols < uint32_t(nacc * cols)) tcols <<= 1;
-  CUtensorMap tu, td;
+  CUtensorMap tu, td, tr;
   int rc = make_map(&tu, c->in[1].ptr, d->nel, NP, BM);
   if (rc) return rc;
-  rc = make_map(&td, c->in[0].ptr, (int64_t)nmat_all * NP, NP, NP);
+  rc = make_map(&td, c->in[0].ptr, (int64_t)nmat_all * NP, NP, C::DM_ROWS);
   if (rc) return rc;
-  CUtensorMap tr;
   rc = make_res_map(&tr, c->out[0].ptr, d->nel, NP, nmat_all);
   if (rc) return rc;
-  const int64_t ntiles = (d->nel + BM - 1) / BM;
-  const int64_t per_group = std::min<int64_t>(ntiles, std::max(1, c->sm_count / groups));
-  const int grid = (int)(per_group * groups);
-  dg_tc_kernel<NP><<<grid, 192, smem, c->stream>>>(tu, td, tr, d->nel, nmat, groups, nacc, tcols);
+  const int64_t ntiles = (d->nel + (PAIR ? 2 * BM : BM) - 1) / (PAIR ? 2 * BM : BM);
+  const int units_max = PAIR ? c->sm_count / 2 : c->sm_count;  // CTAs, or pairs
+  const int64_t per_group = std::min<int64_t>(ntiles, std::max(1, units_max / groups));
+  const int units = (int)(per_group * groups);
+  if constexpr (PAIR) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * units);
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, dg_tc_kernel<NP, true>, tu, td, tr, d->nel, nmat, groups, nacc, tcols);
+    if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "dg_diff_tc pair launch: %s", cudaGetErrorString(e));
+  } else {
+    dg_tc_kernel<NP, false><<<units, 192, smem, c->stream>>>(tu, td, tr, d->nel, nmat, groups, nacc, tcols);
+  }
   return PS_OK;
+}
+
+template <int NP>
+int launch_np(Ctx* c, const ps_kernel_desc* d) {
+  // CTA pairs (opt-in) where the single-CTA kernel splits the matrices into groups
+  if (NP >= 112 && dg_pair_enabled()) return launch_cfg<NP, true>(c, d);
+  return launch_cfg<NP, false>(c, d);
 }
 
 }  // namespace

@@ -66,3 +66,13 @@ def test_dg_tc_matrix_groups(dev, np_, nmat):
     ins = make_inputs(d, io, "seed17")
     np.testing.assert_array_equal(dev.run(d, ins)[0].view(np.uint32),
                                   oracle_suite.run(d, io, ins)[0].view(np.uint32))
+
+
+@pytest.mark.parametrize("nel,np_,nmat", [(1040, 128, 3), (40000, 112, 3), (272, 128, 4)])
+def test_dg_tc_cta_pairs(dev, monkeypatch, nel, np_, nmat):
+    # cta_group::2 path (opt-in, PS_DGTC_PAIR=1): M = 256 tiles, dm split by N
+    monkeypatch.setenv("PS_DGTC_PAIR", "1")
+    d, io = desc_io(_id(nel, np_, nmat))
+    ins = make_inputs(d, io, "seed17")
+    np.testing.assert_array_equal(dev.run(d, ins)[0].view(np.uint32),
+                                  oracle_suite.run(d, io, ins)[0].view(np.uint32))
