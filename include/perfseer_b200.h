@@ -24,6 +24,17 @@
  *   ps_eval_batched
  *       perfseer::predict + report ranking     src/model.cpp:615-623,
  *                                              tools/perfseer.cpp:452-469
+ *   ps_run_host / ps_run_host_batch
+ *       `perfseer measure` over a kernel directory through host data
+ *       (tools/perfseer.cpp:211-240), one kernel / a pipelined sweep
+ *   ps_enumerate
+ *       perfseer::brute_force_count            src/oracle.cpp:76-425
+ *   ps_catalog / ps_feature_table / ps_fit_cpu / ps_predict_cpu / ...
+ *       the C++ port's KernelCollection::generate, gather_feature_values,
+ *       fit_model, predict (uipick.cpp:71-119, features.cpp:417-493,
+ *       model.cpp:485-623) for non-C++ hosts
+ *   ps_prepare / ps_trim / ps_mark / ps_elapsed / ps_host_alloc
+ *       new: residency, step timing and pinned staging for the B200 sweep
  *
  * Threading: one ps_ctx per GPU; a ps_ctx must not be used concurrently
  * (executors are exclusive resources, executor.hpp:13-15).
