@@ -2,8 +2,7 @@
 for every suite kernel, its binding resource, achieved rate and fraction of
 that resource's peak, and the best fraction per kernel family.
 
-  HBM       gmem_pattern, overlap_knl, finite_diff(_rm), dg_diff_rm keep-res,
-            dg_diff_tc: algorithmic bytes (ps_kernel_io.bytes_global) / time
+  HBM       gmem_pattern, overlap_knl, finite_diff(_rm), dg_diff_tc: algorithmic bytes (ps_kernel_io.bytes_global) / time
             vs MEASURED_PEAKS.json hbm_gbs
   FP32      flops_*_pattern: 2048 m E ops (madd counted once) / time vs
             148 SMs x 128 lanes x clock
@@ -12,8 +11,10 @@ that resource's peak, and the best fraction per kernel family.
             madd x 4 B / time vs 148 x 128 B/clk x clock
   tensor    matmul_sq_tc: 2 n^3 / time vs MEASURED bf16 / 2
   latency   barrier_knl, empty_knl: absolute (no throughput roofline)
-  wr        matmul_sq_rm, dg_diff_rm keep u/dm: work-removed calibration
-            kernels, timed only (no roofline claim)
+  wr        matmul_sq_rm, dg_diff_rm: work-removed calibration kernels that
+            time one access pattern of an application kernel as that kernel
+            issues it (e.g. DG's res stores, stride Np across lanes), timed
+            only (no roofline claim)
 
 usage: python tools/roofline_table.py TABLE.csv [--clock-mhz 1965] [--csv OUT]
 """
@@ -36,8 +37,7 @@ DG_BYTES_PER_MADD = {0: 8.0, 1: 4.0 + 4.0 / 3.0, 2: 8.0, 3: 8.0}
 def classify(vid: str, d, io, t: float, clk_hz: float, peaks: dict) -> tuple[str, float, float, str]:
     sm = 148
     gen = vid.split("__")[0]
-    if gen in ("gmem_pattern", "overlap_knl", "finite_diff", "finite_diff_rm", "dg_diff_tc") or (
-            gen == "dg_diff_rm" and "keep-res" in vid):
+    if gen in ("gmem_pattern", "overlap_knl", "finite_diff", "finite_diff_rm", "dg_diff_tc"):
         return "hbm", io.bytes_global / t / 1e9, peaks["hbm_gbs"], "GB/s"
     if gen.startswith("flops_"):
         ops = io.flops / (2.0 if "madd" in gen else 1.0)
@@ -53,7 +53,7 @@ def classify(vid: str, d, io, t: float, clk_hz: float, peaks: dict) -> tuple[str
         return "tensor", io.flops / t / 1e12, peaks["bf16_tflops"] / 2.0, "TFLOP/s"
     if gen in ("barrier_knl", "empty_knl"):
         return "latency", t * 1e6, float("nan"), "us"
-    # work-removed kernels (matmul_sq_rm, dg_diff_rm keep u/dm): timed for
+    # work-removed kernels (matmul_sq_rm, dg_diff_rm): timed for
     # calibration only, no throughput claim; bytes_global / time for reference
     return "wr", io.bytes_global / t / 1e9, float("nan"), "GB/s"
 
