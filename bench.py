@@ -777,6 +777,15 @@ def run_ours(args, dist: Dist) -> None:
     elapsed_max = dist.max(elapsed)
     table = dist.gather_table(records)
 
+    # cross-rank timing agreement (SURVEY 8(e) caveat): every rank times the
+    # same HBM stream; the table is only comparable across GPUs if they agree
+    ref_vid = ("gmem_pattern__dtype-float32__lid_stride_0-1__lid_stride_1-2048__lsize_0-16"
+               "__lsize_1-16__n_input_arrays-2__nelements-268435456")
+    ref_mean, _ = dev.measure_summary(desc_from_id(ref_vid), trials=10, warmup=2)
+    per_rank = dist.all_gather_rows(np.array([[ref_mean]]))[:, 0]
+    cross_rank = {"kernel": ref_vid, "seconds_per_rank": [round(float(x), 9) for x in per_rank],
+                  "max_over_min": round(float(per_rank.max() / per_rank.min()), 4)}
+
     # e2e through host buffers (ps_run_host: H2D + kernel + D2H per launch)
     e2e_set = [i for i in my_kernels
                if not (descs[i].gen in (1, 6) and descs[i].nelements > (1 << 28))]
@@ -983,6 +992,7 @@ def run_ours(args, dist: Dist) -> None:
                         "outputs D2H, pipelined over two device slots (copy-in, launch, copy-out "
                         "streams)"},
         "gpu_launches": int(len(table) + args.steps * len(e2e_set)),
+        "cross_rank_timing": cross_rank,
         "clocks": clocks,
         "host_wall_s": round(wall, 3),
     }
