@@ -507,17 +507,33 @@ __global__ void __launch_bounds__(FD_STRIP_THREADS) finite_diff_strip(const floa
 #pragma unroll
         for (int j = 0; j < QJ; ++j) {
           const int c = 4 * (lane + 32 * j);
-          if (c >= width) continue;
+          if (4 * 32 * j >= width) continue;  // warp-uniform: the whole chunk is past the strip
+          const bool live = c < width;
           float o[4] = {0.0f, 0.0f, 0.0f, 0.0f};
           if constexpr (MODE == 0) {
-            // rows r, r+1, r+2 over columns c .. c+7 (two aligned float4 each)
-            const float4* q0 = reinterpret_cast<const float4*>(&reg[r][c]);
-            const float4* q1 = reinterpret_cast<const float4*>(&reg[r + 1][c]);
-            const float4* q2 = reinterpret_cast<const float4*>(&reg[r + 2][c]);
-            const float4 a0 = q0[0], b0 = q0[1], a1 = q1[0], b1 = q1[1], a2 = q2[0], b2 = q2[1];
-            const float x0[4] = {a0.y, a0.z, a0.w, b0.x};
-            const float x1[6] = {a1.x, a1.y, a1.z, a1.w, b1.x, b1.y};
-            const float x2[4] = {a2.y, a2.z, a2.w, b2.x};
+            // rows r, r+1, r+2 over columns c .. c+5: the lane's aligned
+            // float4 of each row; the two columns past it come from the next
+            // lane's float4 (shuffle) — lane 31 reads them itself — so each
+            // row is read once from shared memory instead of twice
+            float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0;
+            if (c < width + 4) {  // the first lane past the strip supplies the halo columns
+              a0 = *reinterpret_cast<const float4*>(&reg[r][c]);
+              a1 = *reinterpret_cast<const float4*>(&reg[r + 1][c]);
+              a2 = *reinterpret_cast<const float4*>(&reg[r + 2][c]);
+            }
+            float n0 = __shfl_down_sync(0xffffffffu, a0.x, 1);
+            float n1 = __shfl_down_sync(0xffffffffu, a1.x, 1);
+            float n1b = __shfl_down_sync(0xffffffffu, a1.y, 1);
+            float n2 = __shfl_down_sync(0xffffffffu, a2.x, 1);
+            if (lane == 31 && live) {
+              n0 = reg[r][c + 4];
+              n1 = reg[r + 1][c + 4];
+              n1b = reg[r + 1][c + 5];
+              n2 = reg[r + 2][c + 4];
+            }
+            const float x0[4] = {a0.y, a0.z, a0.w, n0};
+            const float x1[6] = {a1.x, a1.y, a1.z, a1.w, n1, n1b};
+            const float x2[4] = {a2.y, a2.z, a2.w, n2};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               float t = __fadd_rn(x0[k], x1[k]);
@@ -526,6 +542,7 @@ __global__ void __launch_bounds__(FD_STRIP_THREADS) finite_diff_strip(const floa
               o[k] = __fadd_rn(t, x2[k]);
             }
           }
+          if (!live) continue;
           float* dst = rbase + (int64_t)r * n + c;
           if (c + 3 < width) {
             __stcs(reinterpret_cast<float4*>(dst), make_float4(o[0], o[1], o[2], o[3]));
