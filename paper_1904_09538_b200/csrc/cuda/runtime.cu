@@ -666,7 +666,7 @@ int launch(Ctx* c, const ps_kernel_desc* d) {
       const int I = d->tile - 2;
       const int groups = n / I;
       dim3 block(d->tile, d->tile);
-      dim3 sblock(FD_STRIP_THREADS);
+      dim3 sblock(d->tile == 16 ? fd_strip_threads<16>() : fd_strip_threads<18>());
       // widest strip that still leaves >= 8 CTAs per SM to schedule (wide
       // strips keep more loads in flight per thread; narrow ones fill the
       // 148 SMs on small grids)
@@ -699,7 +699,8 @@ int launch(Ctx* c, const ps_kernel_desc* d) {
       const int groups = n / I;
       const int64_t want = 8LL * c->sm_count;
       const int R = (d->keep == PS_KEEP_U && (int64_t)(groups + 15) / 16 * groups >= want) ? 16 : 8;
-      dim3 grid((groups + R - 1) / R, groups), block(FD_STRIP_THREADS);
+      dim3 grid((groups + R - 1) / R, groups),
+          block(d->tile == 16 ? fd_strip_threads<16>() : fd_strip_threads<18>());
       if (d->keep == PS_KEEP_U) {
         if (d->tile == 16) {
           if (R == 16)

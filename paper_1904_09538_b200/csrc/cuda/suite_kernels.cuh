@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(T* T) finite_diff_multi(const float* __restric
   }
 }
 
-// K12/K13, strip realisation: one CTA of FD_STRIP_THREADS threads owns R
+// K12/K13, strip realisation: one CTA of fd_strip_threads<T>() threads owns R
 // horizontally adjacent work-groups, i.e. the u strip rows I*i_out ..
 // I*i_out+T-1, columns I*R*bx .. I*R*bx + I*R + 1. The union of the R tiles
 // (every work-item's fetch: the overlapping halo columns are the same u
@@ -449,14 +449,19 @@ __global__ void __launch_bounds__(T* T) finite_diff_multi(const float* __restric
 // group is not a whole number of warps).
 // MODE 0: finite_diff; 1: finite_diff_rm keep u (tgt_read_dest tiles);
 // 2: finite_diff_rm keep res (res interior = tgt_read = 0).
-constexpr int FD_STRIP_THREADS = 256;
+// 7 warps for 16x16 tiles and 8 for 18x18: each warp then owns exactly
+// I / NW = 2 interior rows of the strip
+template <int T>
+constexpr int fd_strip_threads() {
+  return T == 16 ? 224 : 256;
+}
 
 template <int T, int R, int MODE>
-__global__ void __launch_bounds__(FD_STRIP_THREADS) finite_diff_strip(const float* __restrict__ u,
-                                                                     float* __restrict__ out, int n) {
+__global__ void __launch_bounds__(fd_strip_threads<T>()) finite_diff_strip(const float* __restrict__ u,
+                                                                          float* __restrict__ out, int n) {
   constexpr int I = T - 2;
-  constexpr int SW = I * R + 2;             // strip width
-  constexpr int NW = FD_STRIP_THREADS / 32;  // warps
+  constexpr int SW = I * R + 2;                   // strip width
+  constexpr int NW = fd_strip_threads<T>() / 32;  // warps
   constexpr int CJ = (SW + 31) / 32;         // 32-column chunks per strip row
   constexpr int RW = (T + NW - 1) / NW;      // strip rows per warp (upper bound)
   // row pitch: a multiple of 4 floats so that every strip row starts 16-byte
