@@ -75,8 +75,13 @@ __global__ void __launch_bounds__(128) eval_points_kernel(FlatTables t, const in
           acc += term;
         }
         const long long den = t.feat_den[slot];
+        const __int128 lim = (__int128)1 << 53;
         if (den == 1) {
           f[j] = (double)acc;
+        } else if (acc < lim && acc > -lim && den < (1LL << 53)) {
+          // both exact doubles: one correctly rounded division of the same
+          // real quotient the lowest-terms form divides, so the same bits
+          f[j] = (double)(long long)acc / (double)den;
         } else {  // Rational -> double as the host does: lowest terms, one division
           __int128 a = acc < 0 ? -acc : acc, b = den;
           while (b) {
