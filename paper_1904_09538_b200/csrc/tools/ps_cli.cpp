@@ -5,7 +5,8 @@
 //   count      symbolic counts of one kernel (+ values at --bind)
 //   generate   expand catalog kernels from filter tags into a directory
 //   measure    time a kernel directory on --device (synthetic spec JSON, or
-//              cuda:<N> for the sm_100a executor behind ps_measure)
+//              cuda:<N>[,<N>...] for the sm_100a executor behind ps_measure,
+//              one host thread and context per GPU, LPT-sharded)
 //   features   evaluate a model's input features over a kernel directory
 //   calibrate  fit a model to a feature table + measurement CSV
 //   predict    predicted seconds for one kernel or a directory
@@ -25,12 +26,15 @@
 #include <functional>
 #include <iostream>
 #include <map>
+#include <optional>
+#include <thread>
 #include <memory>
 #include <set>
 #include <sstream>
 #include <string>
 #include <vector>
 
+#include "../../../include/perfseer_b200.h"
 #include "json.hpp"
 #include "ps_catalog.hpp"
 #include "ps_counting.hpp"
@@ -289,37 +293,104 @@ int run_generate(const Args& a, const Globals& g) {
 // measure: a synthetic device spec (the reference's CPU test double) or the
 // B200 executor ("cuda:<N>")
 
+// Estimated seconds of one trial of a catalog kernel (for sharding only).
+double estimate_seconds(const std::string& id) {
+  ps_kernel_desc d;
+  ps_io_info io;
+  if (ps_desc_from_id(id.c_str(), &d) != PS_OK || ps_kernel_io(&d, &io) != PS_OK) return 1e-5;
+  return io.bytes_global / 6.0e12 + io.flops / 30e12 + io.bytes_shared / 30e12 + 4e-6;
+}
+
+// `--device cuda:0,1,...`: one CudaExecutor (one ps_ctx) per GPU, each driven
+// by its own host thread (ABI threading contract: one context per GPU, not
+// reentrant); kernels are LPT-balanced over the GPUs on their estimated time,
+// and the records are merged back into directory order.
+std::vector<int> cuda_devices(const std::string& dev) {
+  std::vector<int> out;
+  std::stringstream ss(dev.substr(5));
+  for (std::string tok; std::getline(ss, tok, ',');) out.push_back(std::stoi(tok));
+  if (out.empty()) throw Error("--device cuda:<N>[,<N>...] lists no device");
+  return out;
+}
+
 int run_measure(const Args& a, const Globals& g) {
   const std::string dev = a.one("device");
   const int trials = std::stoi(a.one("trials", "60"));
-  std::unique_ptr<Executor> ex;
   std::map<std::string, std::string> hashes;
+  const KernelDir kd = read_kernel_dir(a.one("kernels"));
+  const size_t nk = kd.kernels.size();
+  std::vector<std::optional<MeasurementRecord>> recs(nk);
+  std::vector<std::string> errs(nk);
+  std::string dev_id;
   if (dev.rfind("cuda:", 0) == 0) {
     const int warmup = std::stoi(a.one("warmup", "5"));
-    ex = std::make_unique<CudaExecutor>(std::stoi(dev.substr(5)), warmup);
+    const std::vector<int> gpus = cuda_devices(dev);
     hashes["device"] = file_hash_hex(dev);
+    // LPT: longest first onto the least-loaded GPU
+    std::vector<size_t> order(nk);
+    for (size_t i = 0; i < nk; ++i) order[i] = i;
+    std::vector<double> est(nk);
+    for (size_t i = 0; i < nk; ++i) est[i] = estimate_seconds(kd.kernels[i].id);
+    std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return est[x] > est[y]; });
+    std::vector<std::vector<size_t>> shard(gpus.size());
+    std::vector<double> load(gpus.size(), 0.0);
+    for (size_t i : order) {
+      const size_t r = std::min_element(load.begin(), load.end()) - load.begin();
+      shard[r].push_back(i);
+      load[r] += est[i];
+    }
+    std::vector<std::string> ids(gpus.size());
+    std::vector<std::string> init_err(gpus.size());
+    std::vector<std::thread> pool;
+    for (size_t r = 0; r < gpus.size(); ++r)
+      pool.emplace_back([&, r] {
+        try {
+          CudaExecutor ex(gpus[r], warmup);
+          ids[r] = ex.id();
+          for (size_t i : shard[r]) {
+            const auto& ki = kd.kernels[i];
+            try {
+              MeasurementRecord rec = measure_kernel(ex, ki.kernel, ki.bindings, trials);
+              rec.kernel_id = ki.id;
+              recs[i] = std::move(rec);
+            } catch (const std::exception& e) {
+              errs[i] = ki.id + ": " + e.what();
+            }
+          }
+        } catch (const std::exception& e) {
+          init_err[r] = e.what();
+          for (size_t i : shard[r]) errs[i] = kd.kernels[i].id + ": " + e.what();
+        }
+      });
+    for (auto& t : pool) t.join();
+    for (size_t r = 0; r < gpus.size(); ++r) dev_id += (r ? "+" : "") + (ids[r].empty() ? "cuda_b200_?" : ids[r]);
   } else {
     SyntheticDeviceSpec spec = SyntheticDeviceSpec::from_json_string(slurp(dev));
     if (g.seed_given) spec.seed = static_cast<uint64_t>(g.seed);
-    ex = std::make_unique<SyntheticDevice>(spec);
+    SyntheticDevice ex(spec);
     hashes["device"] = hash_of(dev);
-  }
-  const KernelDir kd = read_kernel_dir(a.one("kernels"));
-  std::vector<MeasurementRecord> recs;
-  std::vector<std::string> failures;
-  for (const auto& ki : kd.kernels) {
-    try {
-      MeasurementRecord r = measure_kernel(*ex, ki.kernel, ki.bindings, trials);
-      r.kernel_id = ki.id;
-      recs.push_back(std::move(r));
-    } catch (const Error& e) {
-      failures.push_back(ki.id + ": " + e.what());
+    dev_id = ex.id();
+    for (size_t i = 0; i < nk; ++i) {
+      const auto& ki = kd.kernels[i];
+      try {
+        MeasurementRecord rec = measure_kernel(ex, ki.kernel, ki.bindings, trials);
+        rec.kernel_id = ki.id;
+        recs[i] = std::move(rec);
+      } catch (const Error& e) {
+        errs[i] = ki.id + ": " + e.what();
+      }
     }
   }
+  std::vector<MeasurementRecord> ok;
+  std::vector<std::string> failures;
+  for (size_t i = 0; i < nk; ++i) {
+    if (recs[i]) ok.push_back(std::move(*recs[i]));
+    if (!errs[i].empty()) failures.push_back(errs[i]);
+  }
   std::string head = make_manifest("measure", hashes, g.seed_given ? g.seed : 0).comment_line() + "\n";
-  head += "# device: " + ex->id() + ", trials: " + std::to_string(trials) + "\n";
+  head += "# device: " + dev_id + ", trials: " + std::to_string(trials) + "\n";
   for (const auto& f : failures) head += "# failed: " + f + "\n";
-  spit(a.one("out"), head + measurements_to_csv(recs));
+  spit(a.one("out"), head + measurements_to_csv(ok));
   for (const auto& f : failures) std::cerr << "failed: " << f << "\n";
   return failures.empty() ? 0 : 2;
 }
@@ -538,7 +609,7 @@ const std::vector<Command>& commands() {
        {{"tag", "tags", "match", "out", "catalog"}, {}, {"out"}},
        run_generate},
       {"measure",
-       "run kernels on an executor (synthetic spec JSON or cuda:<N>)",
+       "run kernels on an executor (synthetic spec JSON or cuda:<N>[,<N>...])",
        {{"device", "kernels", "trials", "warmup", "out"}, {}, {"device", "kernels", "out"}},
        run_measure},
       {"features",

@@ -172,3 +172,19 @@ def test_measure_on_b200(cli, tmp_path):
     assert lines[1] == "# device: cuda_b200_0, trials: 10"
     rows = list(csv.DictReader(l for l in lines if not l.startswith("#")))
     assert len(rows) == 2 and all(0 < float(r["mean_seconds"]) < 1 for r in rows)
+
+
+@pytest.mark.gpu
+def test_measure_threads_per_gpu(cli, tmp_path):
+    # one host thread + context per listed device, LPT-sharded; two contexts on
+    # GPU 0 exercise the threaded path on a one-GPU box
+    run("generate", "--catalog", "b200", "--tag", "finite_diff", "--tag", "n:1120,2240", "--out", "k",
+        cwd=tmp_path)
+    run("measure", "--device", "cuda:0,0", "--kernels", "k", "--trials", 5, "--warmup", 1,
+        "--out", "meas.csv", cwd=tmp_path)
+    lines = (tmp_path / "meas.csv").read_text().splitlines()
+    assert lines[1] == "# device: cuda_b200_0+cuda_b200_0, trials: 5"
+    rows = list(csv.DictReader(l for l in lines if not l.startswith("#")))
+    man = json.loads((tmp_path / "k" / "manifest.json").read_text())
+    assert [r["kernel"] for r in rows] == [k["id"] for k in man["kernels"]]  # directory order
+    assert all(0 < float(r["mean_seconds"]) < 1 for r in rows)
