@@ -903,6 +903,12 @@ def run_ours(args, dist: Dist) -> None:
 
     dom = max(share, key=share.get)
     roofline = roofline_of(dom)
+    # every kernel family against its binding resource (best size per family)
+    from paper_1904_09538_b200.rooflines import best_per_family, rows_of
+    suite_rooflines = {fam: {"bound": r[1], "achieved": round(r[2], 2), "peak": round(r[3], 2),
+                             "unit": r[4], "frac": round(r[5], 4), "kernel": r[0]}
+                       for fam, r in sorted(best_per_family(
+                           rows_of(mean_s, sm_mhz * 1e6, pk)).items())}
     gm = [k for k in trials if descs[k].gen == 1]
     roofline_hbm = roofline_of(max(gm, key=lambda k: ios[k].bytes_global)) if gm else None
 
@@ -982,6 +988,7 @@ def run_ours(args, dist: Dist) -> None:
         "tensor_variant": tensor_variant,
         "overlap_diagnosis": diagnosis,
         "roofline_hbm": roofline_hbm,
+        "suite_rooflines": suite_rooflines,
         "cpu_baseline": cpu_gmem_sample() if dist.world == 1 else None,
         # the reference library itself on the host cores (modelling path)
         "cpu_baseline_reference": reference_model_sample() if dist.world == 1 else None,
