@@ -971,7 +971,8 @@ def run_ours(args, dist: Dist) -> None:
                    "l2": "no flush: every kernel's trials run back to back as the reference's "
                          "measure_kernel times them (executor.cpp:40-48; warm caches for the small "
                          "application sizes are part of what the model predicts); the HBM "
-                         "microbenchmarks and the large sizes use arrays >= 1 GiB (> 126 MB L2)",
+                         "microbenchmarks use arrays >= 1 GiB and the largest application sizes "
+                         "exceed the 126 MB L2 (matmul 8192: 256 MB per array, DG 10^6: 0.25-2 GB)",
                    "parallelism": f"(kernel, trial) units LPT-sharded over {dist.world} rank(s)"},
         "suite_hbm_GBps": round(hbm_b / hbm_t / 1e9, 1) if hbm_t else None,
         "suite_flops_TFps": round(fl / fl_t / 1e12, 2) if fl_t else None,
