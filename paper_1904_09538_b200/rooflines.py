@@ -30,7 +30,8 @@ def classify(vid: str, d, io, t: float, clk_hz: float, peaks: dict) -> tuple[str
     if gen in ("gmem_pattern", "overlap_knl", "finite_diff", "finite_diff_rm", "dg_diff_tc"):
         return "hbm", io.bytes_global / t / 1e9, peaks["hbm_gbs"], "GB/s"
     if gen.startswith("flops_"):
-        ops = io.flops / (2.0 if "madd" in gen else 1.0)
+        # instructions: a madd is one FFMA (io.flops counts it as 2 flops)
+        ops = io.flops - (2048.0 * float(d.m) * float(d.nelements) if "madd" in gen else 0.0)
         return "fp32", ops / t / 1e12, sm * 128 * clk_hz / 1e12, "Tops/s"
     if gen == "lmem_shuffle":
         return "shared", io.bytes_shared / t / 1e12, sm * 128 * clk_hz / 1e12, "TB/s"
