@@ -660,6 +660,10 @@ def run_reference_arm(args, dist: Dist) -> None:
     if dist.rank != 0:
         return
     from oracle import suite as oracle_suite
+    if dist.world > 1:
+        # torchrun pins OMP_NUM_THREADS=1 per rank; rank 0 runs the reference
+        # alone here, with every host thread
+        oracle_suite.set_threads(os.cpu_count() or 1)
     from paper_1904_09538_b200 import desc_from_id, kernel_io
     _, kernels = workload_kernels(args.workload)
     sample = []

@@ -26,6 +26,7 @@ def lib() -> C.CDLL:
         _lib.ref_flops_value.restype = C.c_float
         _lib.ref_flops_value.argtypes = [C.c_int, C.c_int64]
         _lib.ref_threads.restype = C.c_int
+        _lib.ref_set_threads.argtypes = [C.c_int]
     return _lib
 
 
@@ -66,3 +67,7 @@ def run(desc, io, inputs: list[np.ndarray]) -> list[np.ndarray]:
 
 def threads() -> int:
     return lib().ref_threads()
+
+
+def set_threads(n: int) -> None:
+    lib().ref_set_threads(n)
