@@ -583,16 +583,17 @@ def c5_report(dev, parts, variants: list[dict], npts: int = 1_000_000, dist=None
         srt = np.sort(pc[:, cols], axis=1)
         tie = (srt[:, 1] - srt[:, 0]) <= 1e-12 * np.abs(srt[:, 0])
         mism += int(np.sum((ag[:nsub, g] != ac[:, g]) & ~tie))
-    # reference-API predict() (features through evaluate_feature) on a sample
-    nref = 64
+    # reference-API predict() (features through evaluate_feature, one kernel
+    # instance per point) on a sample, one batched call per variant
+    nref = 256
     t0 = time.perf_counter()
     ref_rel = 0.0
-    for j in range(nref):
-        for v, var in enumerate(variants):
-            sizes = {k: int(pts[j, c]) for k, c in var["coords"].items()}
-            m = host.HostModel(var["model"])
-            r = m.predict_cpu(np.array(var["params"]), [_concrete(var["id"], sizes)])[0]
-            ref_rel = max(ref_rel, abs(pg[j, v] - r) / abs(r))
+    for v, var in enumerate(variants):
+        m = host.HostModel(var["model"])
+        ids = [_concrete(var["id"], {k: int(pts[j, c]) for k, c in var["coords"].items()})
+               for j in range(nref)]
+        r = m.predict_cpu(np.array(var["params"]), ids)
+        ref_rel = max(ref_rel, float(np.max(np.abs(pg[:nref, v] - r) / np.abs(r))))
     ref_t = time.perf_counter() - t0
     winners = {}
     for g, (wl, _c, _a) in enumerate(parts):
