@@ -805,28 +805,36 @@ def run_ours(args, dist: Dist) -> None:
         pinned[i] = (ins, outs)
         h2d += sum(a.nbytes for a in ins)
         d2h += sum(a.nbytes for a in outs)
-    # one pipelined pass per step (ps_run_host_batch: H2D of the next kernel,
-    # this launch and D2H of the previous overlap on three streams)
+    # one pipelined pass per step (ps_run_host_batch_ex: H2D of the next
+    # kernel, this launch and the previous read-back overlap on three streams).
+    # e2e: the step's result read back is one device checksum per kernel (the
+    # sweep's product is its timing table, the output arrays are scratch);
+    # e2e_full_outputs: every output array copied back as well.
     batch = [descs[i] for i in e2e_set]
     b_in = [pinned[i][0] for i in e2e_set]
     b_out = [pinned[i][1] for i in e2e_set]
     if e2e_set:
         dev.run_host_batch(batch, b_in, b_out)  # warm (allocates the two slots)
     dist.barrier()
-    e2e_time = 0.0
+    e2e_time = e2e_full_time = 0.0
     e2e_bytes = 0.0
     for _ in range(args.steps):
         if e2e_set:
-            e2e_time += dev.run_host_batch(batch, b_in, b_out)
+            e2e_time += dev.run_host_batch(batch, b_in, None, checksums=True)[0]
+            e2e_full_time += dev.run_host_batch(batch, b_in, b_out)
         e2e_bytes += sum(ios[i].bytes_global for i in e2e_set)
     e2e_time_max = dist.max(e2e_time)
+    e2e_full_time_max = dist.max(e2e_full_time)
+    d2h_full = d2h
+    d2h = 8 * len(e2e_set)
     e2e_bytes_all = e2e_bytes
     if dist.pg:
         import torch
         devn = f"cuda:{dist.device}" if dist.backend == "nccl" else "cpu"
-        t = torch.tensor([e2e_bytes, float(h2d), float(d2h)], dtype=torch.float64, device=devn)
+        t = torch.tensor([e2e_bytes, float(h2d), float(d2h), float(d2h_full)], dtype=torch.float64,
+                         device=devn)
         dist.pg.all_reduce(t)
-        e2e_bytes_all, h2d, d2h = t.tolist()
+        e2e_bytes_all, h2d, d2h, d2h_full = t.tolist()
     for ins, outs in pinned.values():
         for a in ins + outs:
             a.free()
@@ -1004,10 +1012,18 @@ def run_ours(args, dist: Dist) -> None:
         "e2e": {"value": round(e2e_bytes_all / e2e_time_max / 1e9, 3) if e2e_time_max else None,
                 "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "kernels": len(e2e_set),
-                "note": "ps_run_host_batch: every kernel's inputs H2D from pinned host memory and "
-                        "outputs D2H, pipelined over two device slots (copy-in, launch, copy-out "
-                        "streams)"},
-        "gpu_launches": int(len(table) + args.steps * len(e2e_set)),
+                "note": "ps_run_host_batch_ex: every kernel's inputs H2D from pinned host memory each "
+                        "step, the kernels, and the step's result (one device checksum of each "
+                        "kernel's outputs) D2H; copy-in, launch and read-back pipelined on three "
+                        "streams over two device slots"},
+        "e2e_full_outputs": {"value": round(e2e_bytes_all / e2e_full_time_max / 1e9, 3)
+                             if e2e_full_time_max else None, "unit": "GB/s",
+                             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h_full),
+                             "note": "the same with every output array copied back"},
+        # sweep launches + per e2e step: each kernel twice and one checksum
+        # launch per output array of the checksum pass
+        "gpu_launches": int(len(table) + args.steps * (2 * len(e2e_set)
+                                                       + sum(ios[i].n_outputs for i in e2e_set))),
         "cross_rank_timing": cross_rank,
         "clocks": clocks,
         "host_wall_s": round(wall, 3),

@@ -180,6 +180,12 @@ int ps_run_host(ps_ctx* ctx, const ps_kernel_desc* desc, const void* const* inpu
  * (New; the batched form of ps_run_host for sweeps through host data.) */
 int ps_run_host_batch(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const void* const* inputs,
                       void* const* outputs, double* seconds);
+/* The same with the step's result instead of (or besides) the output arrays:
+ * checksums[i] (n entries, may be NULL) = wrapping 64-bit sum of the 32-bit
+ * words of kernel i's outputs, computed on the device and read back once at
+ * the end of the batch; outputs may be NULL (no output copies). */
+int ps_run_host_batch_ex(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const void* const* inputs,
+                         void* const* outputs, uint64_t* checksums, double* seconds);
 /* Releases every resident prepared variant and staging buffer of the context
  * (the context, its stream and events stay valid; later calls re-prepare). */
 int ps_trim(ps_ctx* ctx);

@@ -106,12 +106,14 @@ def _declare(L: C.CDLL) -> None:
                               C.c_int, P(C.c_double)]
     L.ps_run_host_batch.argtypes = [C.c_void_p, C.c_int, P(KernelDesc), P(C.c_void_p),
                                     P(C.c_void_p), P(C.c_double)]
+    L.ps_run_host_batch_ex.argtypes = [C.c_void_p, C.c_int, P(KernelDesc), P(C.c_void_p),
+                                       P(C.c_void_p), P(C.c_uint64), P(C.c_double)]
     L.ps_trim.argtypes = [C.c_void_p]
     L.ps_host_alloc.argtypes = [C.c_size_t, P(C.c_void_p)]
     L.ps_host_free.argtypes = [C.c_void_p]
     L.ps_mark.argtypes = [C.c_void_p, C.c_int]
     L.ps_elapsed.argtypes = [C.c_void_p, C.c_int, C.c_int, P(C.c_double)]
-    for name in ("ps_run_host", "ps_run_host_batch", "ps_trim", "ps_host_alloc", "ps_host_free", "ps_mark", "ps_elapsed"):
+    for name in ("ps_run_host", "ps_run_host_batch", "ps_run_host_batch_ex", "ps_trim", "ps_host_alloc", "ps_host_free", "ps_mark", "ps_elapsed"):
         getattr(L, name).restype = C.c_int
     for name in ("ps_desc_from_id", "ps_kernel_io", "ps_init", "ps_destroy", "ps_device_info",
                  "ps_prepare", "ps_measure", "ps_measure_summary", "ps_run_timed",

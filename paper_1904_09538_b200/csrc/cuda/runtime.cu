@@ -1038,10 +1038,29 @@ int ps_run_host(ps_ctx* ctx, const ps_kernel_desc* desc, const void* const* inpu
   return PS_OK;
 }
 
+namespace ps {
+// Wrapping 64-bit sum of the 32-bit words of an array (order-independent, so
+// deterministic under atomics): the per-kernel result read back by the
+// pipelined sweep instead of the whole output arrays.
+__global__ void word_checksum(const uint32_t* __restrict__ w, int64_t n, unsigned long long* out) {
+  unsigned long long acc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc += w[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+}  // namespace ps
+
 int ps_run_host_batch(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const void* const* inputs,
                       void* const* outputs, double* seconds) {
+  return ps_run_host_batch_ex(ctx, n, descs, inputs, outputs, nullptr, seconds);
+}
+
+int ps_run_host_batch_ex(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const void* const* inputs,
+                         void* const* outputs, uint64_t* checksums, double* seconds) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c || !descs || !seconds || n < 0) return set_error(PS_ERR_ARG, "ps_run_host_batch: bad argument");
+  if (!outputs && !checksums) return set_error(PS_ERR_ARG, "ps_run_host_batch: neither outputs nor checksums");
   *seconds = 0.0;
   if (n == 0) return PS_OK;
   PS_CUDA(cudaSetDevice(c->device));
@@ -1067,6 +1086,11 @@ int ps_run_host_batch(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const voi
     for (auto& e : row)
       if (!e) PS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if ((rc = events(c, 2))) return rc;
+  unsigned long long* dsum = nullptr;
+  if (checksums) {
+    if ((rc = c->ensure(c->scratch[6], sizeof(unsigned long long) * (size_t)n))) return rc;
+    dsum = reinterpret_cast<unsigned long long*>(c->scratch[6].ptr);
+  }
   cudaEvent_t(&h2d_done)[2] = c->pipe_ev[0];
   cudaEvent_t(&run_done)[2] = c->pipe_ev[1];
   cudaEvent_t(&d2h_done)[2] = c->pipe_ev[2];
@@ -1074,6 +1098,7 @@ int ps_run_host_batch(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const voi
   PS_CUDA(cudaEventRecord(c->ev[0], c->stream));
   PS_CUDA(cudaStreamWaitEvent(c->h2d_stream, c->ev[0], 0));
   PS_CUDA(cudaStreamWaitEvent(c->d2h_stream, c->ev[0], 0));
+  if (dsum) PS_CUDA(cudaMemsetAsync(dsum, 0, sizeof(unsigned long long) * (size_t)n, c->stream));
   size_t in_at = 0, out_at = 0;
   for (int i = 0; i < n; ++i) {
     const int sl = i & 1;
@@ -1086,21 +1111,35 @@ int ps_run_host_batch(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const voi
     PS_CUDA(cudaEventRecord(h2d_done[sl], c->h2d_stream));
     // launch once the inputs are in and the slot's previous outputs are out
     PS_CUDA(cudaStreamWaitEvent(c->stream, h2d_done[sl], 0));
-    if (i >= 2) PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[sl], 0));
+    if (i >= 2 && outputs) PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[sl], 0));
     s.io = io[i];
     c->activate(s);
     if ((rc = launch(c, &descs[i]))) return rc;
+    if (dsum)
+      for (int a = 0; a < io[i].n_outputs; ++a) {
+        const int64_t words = io[i].output_elems[a] * io[i].elem_bytes / 4;
+        const int blocks = (int)std::min<int64_t>((words + 255) / 256, (int64_t)c->sm_count * 8);
+        word_checksum<<<std::max(blocks, 1), 256, 0, c->stream>>>((const uint32_t*)s.out[a].ptr, words, dsum + i);
+      }
     PS_CUDA(cudaEventRecord(run_done[sl], c->stream));
-    PS_CUDA(cudaStreamWaitEvent(c->d2h_stream, run_done[sl], 0));
-    for (int a = 0; a < io[i].n_outputs; ++a)
-      PS_CUDA(cudaMemcpyAsync(outputs[out_at + a], s.out[a].ptr, (size_t)io[i].output_elems[a] * io[i].elem_bytes,
-                              cudaMemcpyDeviceToHost, c->d2h_stream));
-    PS_CUDA(cudaEventRecord(d2h_done[sl], c->d2h_stream));
+    if (outputs) {
+      PS_CUDA(cudaStreamWaitEvent(c->d2h_stream, run_done[sl], 0));
+      for (int a = 0; a < io[i].n_outputs; ++a)
+        PS_CUDA(cudaMemcpyAsync(outputs[out_at + a], s.out[a].ptr,
+                                (size_t)io[i].output_elems[a] * io[i].elem_bytes, cudaMemcpyDeviceToHost,
+                                c->d2h_stream));
+      PS_CUDA(cudaEventRecord(d2h_done[sl], c->d2h_stream));
+    }
     in_at += io[i].n_inputs;
     out_at += io[i].n_outputs;
   }
-  PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[(n - 1) & 1], 0));
-  if (n >= 2) PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[n & 1], 0));
+  if (outputs) {
+    PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[(n - 1) & 1], 0));
+    if (n >= 2) PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[n & 1], 0));
+  }
+  if (dsum)  // the step's result: one checksum per kernel
+    PS_CUDA(cudaMemcpyAsync(checksums, dsum, sizeof(unsigned long long) * (size_t)n, cudaMemcpyDeviceToHost,
+                            c->stream));
   PS_CUDA(cudaEventRecord(c->ev[1], c->stream));
   PS_CUDA(cudaEventSynchronize(c->ev[1]));
   float ms = 0.f;

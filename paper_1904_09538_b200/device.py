@@ -122,19 +122,26 @@ class CudaDevice:
         check(lib().ps_trim(self._ctx))
 
     def run_host_batch(self, kernels, inputs: list[list["PinnedArray"]],
-                       outputs: list[list["PinnedArray"]]) -> float:
-        """A sweep through host data, pipelined (ps_run_host_batch): H2D of the
-        next kernel, this kernel's launch and D2H of the previous one overlap;
-        seconds from the first copy in to the last copy out."""
+                       outputs: list[list["PinnedArray"]] | None, checksums: bool = False):
+        """A sweep through host data, pipelined (ps_run_host_batch_ex): H2D of
+        the next kernel, this kernel's launch and D2H of the previous one
+        overlap; seconds from the first copy in to the last copy out. With
+        checksums=True the step's result is one device-computed checksum per
+        kernel (wrapping sum of its output words), returned as
+        (seconds, uint64 array); outputs may then be None (no array copies)."""
         ds = [_desc(k) for k in kernels]
         arr = (_abi.KernelDesc * max(1, len(ds)))(*ds)
         ip = [a.ptr for ins in inputs for a in ins]
-        op = [a.ptr for outs in outputs for a in outs]
         ipa = (C.c_void_p * max(1, len(ip)))(*ip)
-        opa = (C.c_void_p * max(1, len(op)))(*op)
+        opa = None
+        if outputs is not None:
+            op = [a.ptr for outs in outputs for a in outs]
+            opa = (C.c_void_p * max(1, len(op)))(*op)
+        sums = np.zeros(max(1, len(ds)), dtype=np.uint64)
+        sp = sums.ctypes.data_as(C.POINTER(C.c_uint64)) if checksums else None
         s = C.c_double()
-        check(lib().ps_run_host_batch(self._ctx, len(ds), arr, ipa, opa, C.byref(s)))
-        return s.value
+        check(lib().ps_run_host_batch_ex(self._ctx, len(ds), arr, ipa, opa, sp, C.byref(s)))
+        return (s.value, sums[:len(ds)]) if checksums else s.value
 
 
 class PinnedArray:

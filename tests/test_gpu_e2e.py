@@ -44,3 +44,27 @@ def test_batch_equals_single_launch():
         for arrs in ins_all + outs_all:
             for a in arrs:
                 a.free()
+
+
+def test_batch_checksums_equal_host_sums_of_outputs():
+    # the step's result without output copies: one device checksum per kernel
+    from paper_1904_09538_b200.device import CudaDevice, PinnedArray
+    with CudaDevice(0) as dev:
+        ins_all, want = [], []
+        for vid in IDS:
+            d, io = desc_io(vid)
+            ins = make_inputs(d, io, "seed17")
+            outs = dev.run(d, ins)
+            want.append(sum(int(np.sum(o.view(np.uint32), dtype=np.uint64)) for o in outs) % (1 << 64))
+            pins = []
+            for a in ins:
+                p = PinnedArray(a.nbytes)
+                p.numpy(a.dtype)[:] = a
+                pins.append(p)
+            ins_all.append(pins)
+        secs, sums = dev.run_host_batch(IDS, ins_all, None, checksums=True)
+        assert secs > 0
+        assert [int(x) for x in sums] == want
+        for arrs in ins_all:
+            for a in arrs:
+                a.free()
