@@ -813,8 +813,7 @@ int ps_destroy(ps_ctx* ctx) {
   cudaStreamSynchronize(c->stream);
   for (auto& kv : c->slots) c->release(kv.second);
   c->release(c->host_slot);
-  c->release(c->pipe_slot[0]);
-  c->release(c->pipe_slot[1]);
+  for (auto& ps : c->pipe_slot) c->release(ps);
   for (auto& row : c->pipe_ev)
     for (auto e : row)
       if (e) cudaEventDestroy(e);
@@ -1065,17 +1064,18 @@ int ps_run_host_batch_ex(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const 
   if (n == 0) return PS_OK;
   PS_CUDA(cudaSetDevice(c->device));
   std::vector<ps_io_info> io(n);
-  size_t need[2][2][PS_MAX_ARRAYS] = {};  // [slot][in/out][array] bytes
+  constexpr int NS = Ctx::kPipeSlots;
+  size_t need[NS][2][PS_MAX_ARRAYS] = {};  // [slot][in/out][array] bytes
   int rc;
   for (int i = 0; i < n; ++i) {
     if ((rc = validate_desc(&descs[i])) || (rc = kernel_io(&descs[i], &io[i]))) return rc;
     for (int a = 0; a < io[i].n_inputs; ++a)
-      need[i & 1][0][a] = std::max(need[i & 1][0][a], (size_t)io[i].input_elems[a] * io[i].elem_bytes);
+      need[i % NS][0][a] = std::max(need[i % NS][0][a], (size_t)io[i].input_elems[a] * io[i].elem_bytes);
     for (int a = 0; a < io[i].n_outputs; ++a)
-      need[i & 1][1][a] = std::max(need[i & 1][1][a], (size_t)io[i].output_elems[a] * io[i].elem_bytes);
+      need[i % NS][1][a] = std::max(need[i % NS][1][a], (size_t)io[i].output_elems[a] * io[i].elem_bytes);
   }
   // every allocation before the timed region (cudaMalloc synchronises)
-  for (int sl = 0; sl < 2; ++sl)
+  for (int sl = 0; sl < NS; ++sl)
     for (int a = 0; a < PS_MAX_ARRAYS; ++a) {
       if (need[sl][0][a] && (rc = c->ensure(c->pipe_slot[sl].in[a], need[sl][0][a]))) return rc;
       if (need[sl][1][a] && (rc = c->ensure(c->pipe_slot[sl].out[a], need[sl][1][a]))) return rc;
@@ -1091,9 +1091,9 @@ int ps_run_host_batch_ex(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const 
     if ((rc = c->ensure(c->scratch[6], sizeof(unsigned long long) * (size_t)n))) return rc;
     dsum = reinterpret_cast<unsigned long long*>(c->scratch[6].ptr);
   }
-  cudaEvent_t(&h2d_done)[2] = c->pipe_ev[0];
-  cudaEvent_t(&run_done)[2] = c->pipe_ev[1];
-  cudaEvent_t(&d2h_done)[2] = c->pipe_ev[2];
+  cudaEvent_t(&h2d_done)[NS] = c->pipe_ev[0];
+  cudaEvent_t(&run_done)[NS] = c->pipe_ev[1];
+  cudaEvent_t(&d2h_done)[NS] = c->pipe_ev[2];
   c->prepared = false;
   PS_CUDA(cudaEventRecord(c->ev[0], c->stream));
   PS_CUDA(cudaStreamWaitEvent(c->h2d_stream, c->ev[0], 0));
@@ -1101,17 +1101,17 @@ int ps_run_host_batch_ex(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const 
   if (dsum) PS_CUDA(cudaMemsetAsync(dsum, 0, sizeof(unsigned long long) * (size_t)n, c->stream));
   size_t in_at = 0, out_at = 0;
   for (int i = 0; i < n; ++i) {
-    const int sl = i & 1;
+    const int sl = i % NS;
     Slot& s = c->pipe_slot[sl];
     // copy in once the launch two kernels back has consumed this slot's inputs
-    if (i >= 2) PS_CUDA(cudaStreamWaitEvent(c->h2d_stream, run_done[sl], 0));
+    if (i >= NS) PS_CUDA(cudaStreamWaitEvent(c->h2d_stream, run_done[sl], 0));
     for (int a = 0; a < io[i].n_inputs; ++a)
       PS_CUDA(cudaMemcpyAsync(s.in[a].ptr, inputs[in_at + a], (size_t)io[i].input_elems[a] * io[i].elem_bytes,
                               cudaMemcpyHostToDevice, c->h2d_stream));
     PS_CUDA(cudaEventRecord(h2d_done[sl], c->h2d_stream));
     // launch once the inputs are in and the slot's previous outputs are out
     PS_CUDA(cudaStreamWaitEvent(c->stream, h2d_done[sl], 0));
-    if (i >= 2 && outputs) PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[sl], 0));
+    if (i >= NS && outputs) PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[sl], 0));
     s.io = io[i];
     c->activate(s);
     if ((rc = launch(c, &descs[i]))) return rc;
@@ -1134,8 +1134,7 @@ int ps_run_host_batch_ex(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const 
     out_at += io[i].n_outputs;
   }
   if (outputs) {
-    PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[(n - 1) & 1], 0));
-    if (n >= 2) PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[n & 1], 0));
+    for (int k = std::max(0, n - NS); k < n; ++k) PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[k % NS], 0));
   }
   if (dsum)  // the step's result: one checksum per kernel
     PS_CUDA(cudaMemcpyAsync(checksums, dsum, sizeof(unsigned long long) * (size_t)n, cudaMemcpyDeviceToHost,
@@ -1157,8 +1156,7 @@ int ps_trim(ps_ctx* ctx) {
   c->slots.clear();
   c->cache_bytes = 0;
   c->release(c->host_slot);
-  c->release(c->pipe_slot[0]);
-  c->release(c->pipe_slot[1]);
+  for (auto& ps : c->pipe_slot) c->release(ps);
   c->prepared = false;
   return PS_OK;
 }

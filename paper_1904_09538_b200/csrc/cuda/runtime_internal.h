@@ -44,11 +44,12 @@ struct Ctx {
   DevBuf scratch[8];
   std::map<std::string, Slot> slots;  // keyed by the raw descriptor bytes
   Slot host_slot;                     // caller-data runs (verify / run_host)
-  // ps_run_host_batch: two device slots, copy-in / copy-out streams and the
+  // ps_run_host_batch: kPipeSlots device slots, copy-in / copy-out streams and the
   // per-slot events that order them against the launches on `stream`
-  Slot pipe_slot[2];
+  static constexpr int kPipeSlots = 4;
+  Slot pipe_slot[kPipeSlots];
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
-  cudaEvent_t pipe_ev[3][2] = {};  // [h2d done, launch done, d2h done][slot]
+  cudaEvent_t pipe_ev[3][kPipeSlots] = {};  // [h2d done, launch done, d2h done][slot]
   size_t cache_bytes = 0, cache_cap = 0;
   uint64_t tick = 0;
   bool prepared = false;
