@@ -1015,7 +1015,7 @@ def run_ours(args, dist: Dist) -> None:
                 "note": "ps_run_host_batch_ex: every kernel's inputs H2D from pinned host memory each "
                         "step, the kernels, and the step's result (one device checksum of each "
                         "kernel's outputs) D2H; copy-in, launch and read-back pipelined on three "
-                        "streams over two device slots"},
+                        "streams over four device slots"},
         "e2e_full_outputs": {"value": round(e2e_bytes_all / e2e_full_time_max / 1e9, 3)
                              if e2e_full_time_max else None, "unit": "GB/s",
                              "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h_full),

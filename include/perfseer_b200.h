@@ -174,7 +174,7 @@ int ps_run_host(ps_ctx* ctx, const ps_kernel_desc* desc, const void* const* inpu
                 void* const* outputs, int n_outputs, double* seconds);
 /* End to end over a batch of kernels, pipelined: the H2D copies of kernel
  * i+1, the launch of kernel i and the D2H copies of kernel i-1 overlap (three
- * streams, two device slots; PCIe is full duplex). inputs / outputs hold, for
+ * streams, four device slots; PCIe is full duplex). inputs / outputs hold, for
  * each kernel in order, its n_inputs / n_outputs host pointers (pinned for
  * overlap) back to back. seconds = first H2D to last D2H, CUDA events.
  * (New; the batched form of ps_run_host for sweeps through host data.) */
