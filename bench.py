@@ -814,7 +814,7 @@ def run_ours(args, dist: Dist) -> None:
     b_in = [pinned[i][0] for i in e2e_set]
     b_out = [pinned[i][1] for i in e2e_set]
     if e2e_set:
-        dev.run_host_batch(batch, b_in, b_out)  # warm (allocates the two slots)
+        dev.run_host_batch(batch, b_in, b_out)  # warm (allocates the pipeline slots)
     dist.barrier()
     e2e_time = e2e_full_time = 0.0
     e2e_bytes = 0.0
