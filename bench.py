@@ -919,6 +919,10 @@ def run_ours(args, dist: Dist) -> None:
                                "(SURVEY 8(d) C2; no tensor cores in the paper variants)",
                 "algorithmic_flops_per_launch": ios[k].flops,
                 "share_of_step": round(share[k] / total_t, 4),
+                "traffic_note": ("matmul noPF: DRAM bytes above the 12 n^2 compulsory are b-column "
+                                 "re-streams from L2 misses at ~450 GB/s, not binding; group-M rasters "
+                                 "cut them 60 -> 8.9 GB but run 30-50% slower (L1 a-row sharing), "
+                                 "tools/exp/mm_raster.cu, DESIGN.md K9") if d.gen == 7 else None,
                 "note": "16x16 CUDA-core tiles by construction (uipick.cpp:464-554); the paper "
                         "reports 8-20% of FP32 peak for these variants (PAPER.md:2155-2157)"}
 
