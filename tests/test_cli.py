@@ -105,6 +105,18 @@ def test_count_known_answers(cli, tmp_path):
     assert j["ops"][0]["value"] is None and j["manifest"]["command"] == "count"
 
 
+def test_count_text_kernel(cli, tmp_path):
+    # the text front end (lang.cpp): test_counting.cpp:88-101's
+    # untiled matmul, madd n^3 = 64 at n = 4
+    (tmp_path / "mm.txt").write_text("{[i,j,k]: 0<=i,j,k<n}\nc[i,j] = sum(k, a[i,k]*b[k,j])\n"
+                                     "arg a float32 [n,n]\narg b float32 [n,n]\narg c float32 [n,n]\n")
+    j = json.loads(run("count", "--kernel", "mm.txt", "--bind", "n=4", cwd=tmp_path).stdout)
+    assert j["kernel"] == "mm"
+    assert [(o["op"], o["count"], o["value"]["num"]) for o in j["ops"]] == [("madd", "n^3", "64")]
+    r = run("count", "--kernel", "mm.txt", "--bind", "n", cwd=tmp_path, check=False)
+    assert r.returncode == 1 and "name=value" in r.stderr
+
+
 def test_five_step_workflow_synthetic(cli, tmp_path):
     pipeline(tmp_path)
     cal = json.loads((tmp_path / "cal.json").read_text())
