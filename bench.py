@@ -747,7 +747,11 @@ def run_ours(args, dist: Dist) -> None:
     prev = previous_run_seconds()
     est = [prev.get(k) or estimate_seconds(io) for k, io in zip(kernels, ios)]
     units = [(i, t) for i in range(len(kernels)) for t in range(args.trials_per_step)]
-    mine = lpt(units, est, dist.world)[dist.rank]
+    shards = lpt(units, est, dist.world)
+    mine = shards[dist.rank]
+    # a kernel whose trials are split over ranks runs its e2e pass on exactly
+    # one of them: the rank holding its first trial
+    e2e_owner = {i: r for r, sh in enumerate(shards) for i, t in sh if t == 0}
     my_kernels = sorted({i for i, _ in mine})
 
     dev = CudaDevice(dist.device)
@@ -792,14 +796,29 @@ def run_ours(args, dist: Dist) -> None:
                   "max_over_min": round(float(per_rank.max() / per_rank.min()), 4)}
 
     # e2e through host buffers (ps_run_host: H2D + kernel + D2H per launch)
-    e2e_set = [i for i in my_kernels
-               if not (descs[i].gen in (1, 6) and descs[i].nelements > (1 << 28))]
+    e2e_set = [i for i in my_kernels if e2e_owner.get(i) == dist.rank
+               and not (descs[i].gen in (1, 6) and descs[i].nelements > (1 << 28))]
+    # pinned host memory: ranks on one host share its RAM; the output arrays
+    # (only the e2e_full_outputs pass needs them) are dropped first if the
+    # rank's share would be exceeded
+    import psutil
+    local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    pin_budget = 0.8 * psutil.virtual_memory().available / local_ranks
+    need_in = sum(int(ios[i].input_elems[j]) * ios[i].elem_bytes
+                  for i in e2e_set for j in range(ios[i].n_inputs))
+    need_out = sum(int(ios[i].output_elems[j]) * ios[i].elem_bytes
+                   for i in e2e_set for j in range(ios[i].n_outputs))
+    if need_in > pin_budget:
+        raise SystemExit(f"rank {dist.rank}: e2e inputs need {need_in / 1e9:.1f} GB pinned host "
+                         f"memory, {pin_budget / 1e9:.1f} GB available to this rank")
+    full_outputs = need_in + need_out <= pin_budget
     pinned = {}
     h2d = d2h = 0
     for i in e2e_set:
         io = ios[i]
         ins = [PinnedArray(int(io.input_elems[j]) * io.elem_bytes) for j in range(io.n_inputs)]
-        outs = [PinnedArray(int(io.output_elems[j]) * io.elem_bytes) for j in range(io.n_outputs)]
+        outs = [PinnedArray(int(io.output_elems[j]) * io.elem_bytes)
+                for j in range(io.n_outputs)] if full_outputs else []
         for a in ins:
             a.numpy(np.uint8)[:] = 0x3f
         pinned[i] = (ins, outs)
@@ -821,28 +840,38 @@ def run_ours(args, dist: Dist) -> None:
     batch = [descs[i] for i in e2e_set]
     b_in = [pinned[i][0] for i in e2e_set]
     b_out = [pinned[i][1] for i in e2e_set]
-    if e2e_set:
-        dev.run_host_batch(batch, b_in, b_out)  # warm (allocates the pipeline slots)
+    if e2e_set:  # warm (allocates the pipeline slots)
+        dev.run_host_batch(batch, b_in, None, checksums=True)
+        if full_outputs:
+            dev.run_host_batch(batch, b_in, b_out)
     dist.barrier()
     e2e_time = e2e_full_time = 0.0
     e2e_bytes = 0.0
     for _ in range(args.steps):
         if e2e_set:
             e2e_time += dev.run_host_batch(batch, b_in, None, checksums=True)[0]
-            e2e_full_time += dev.run_host_batch(batch, b_in, b_out)
+            if full_outputs:
+                e2e_full_time += dev.run_host_batch(batch, b_in, b_out)
         e2e_bytes += sum(ios[i].bytes_global for i in e2e_set)
     e2e_time_max = dist.max(e2e_time)
     e2e_full_time_max = dist.max(e2e_full_time)
     d2h_full = d2h
     d2h = 8 * len(e2e_set)
     e2e_bytes_all = e2e_bytes
+    # per step: the checksum pass (each kernel + one checksum per output
+    # array) and, when it runs, the full-output pass
+    e2e_launches = (len(e2e_set) * (2 if full_outputs else 1)
+                    + sum(ios[i].n_outputs for i in e2e_set))
+    e2e_kernels = len(e2e_set)
+    full_all = float(full_outputs)
     if dist.pg:
         import torch
         devn = f"cuda:{dist.device}" if dist.backend == "nccl" else "cpu"
-        t = torch.tensor([e2e_bytes, float(h2d), float(d2h), float(d2h_full)], dtype=torch.float64,
-                         device=devn)
+        t = torch.tensor([e2e_bytes, float(h2d), float(d2h), float(d2h_full), float(e2e_launches),
+                          float(e2e_kernels), 1.0 - full_all], dtype=torch.float64, device=devn)
         dist.pg.all_reduce(t)
-        e2e_bytes_all, h2d, d2h, d2h_full = t.tolist()
+        e2e_bytes_all, h2d, d2h, d2h_full, e2e_launches, e2e_kernels, missing = t.tolist()
+        full_all = float(missing == 0)
     for ins, outs in pinned.values():
         for a in ins + outs:
             a.free()
@@ -1023,19 +1052,20 @@ def run_ours(args, dist: Dist) -> None:
         "cpu_baseline_reference": reference_model_sample() if dist.world == 1 else None,
         "e2e": {"value": round(e2e_bytes_all / e2e_time_max / 1e9, 3) if e2e_time_max else None,
                 "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "kernels": len(e2e_set),
+                "kernels": int(e2e_kernels),
                 "note": "ps_run_host_batch_ex: every kernel's inputs H2D from pinned host memory each "
                         "step, the kernels, and the step's result (one device checksum of each "
                         "kernel's outputs) D2H; copy-in, launch and read-back pipelined on three "
                         "streams over four device slots"},
         "e2e_full_outputs": {"value": round(e2e_bytes_all / e2e_full_time_max / 1e9, 3)
-                             if e2e_full_time_max else None, "unit": "GB/s",
+                             if e2e_full_time_max and full_all else None, "unit": "GB/s",
                              "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h_full),
-                             "note": "the same with every output array copied back"},
-        # sweep launches + per e2e step: each kernel twice and one checksum
-        # launch per output array of the checksum pass
-        "gpu_launches": int(len(table) + args.steps * (2 * len(e2e_set)
-                                                       + sum(ios[i].n_outputs for i in e2e_set))),
+                             "note": "the same with every output array copied back"
+                             + ("" if full_all else " (skipped: output arrays do not fit this "
+                                "host's pinned memory share)")},
+        # sweep launches (all ranks) + per e2e step: every rank's checksum
+        # pass (kernels + checksum launches) and full-output pass
+        "gpu_launches": int(len(table) + args.steps * e2e_launches),
         "cross_rank_timing": cross_rank,
         "clocks": clocks,
         "host_wall_s": round(wall, 3),
