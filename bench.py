@@ -49,7 +49,7 @@ def peaks() -> tuple[dict, str]:
 
 
 class Dist:
-    def __init__(self):
+    def __init__(self, process_group: bool = True):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -58,7 +58,7 @@ class Dist:
         self.device = int(os.environ.get("PS_BENCH_DEVICE", self.local_rank))
         self.pg = None
         self.backend = None
-        if self.world > 1:
+        if self.world > 1 and process_group:
             import torch
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -1090,7 +1090,9 @@ def main() -> None:
     ap.add_argument("--headline-model", default="",
                     help="model whose GPU fit is the headline (default: the workload's)")
     args = ap.parse_args()
-    dist = Dist()
+    # the reference arm is CPU-only with no exchange (rank 0 alone runs it):
+    # no process group, no GPU binding
+    dist = Dist(process_group=args.impl != "reference")
     try:
         if args.impl == "reference":
             run_reference_arm(args, dist)

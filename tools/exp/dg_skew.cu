@@ -173,6 +173,52 @@ __global__ void __launch_bounds__(256) dg_dmpf_ahead(const float* __restrict__ d
   }
 }
 
+// dmPF with 16-byte u loads: lane l loads the tile's four quarters starting
+// at quarter ROT ? (l & 3) : 0 (4 line offsets per instruction at any pitch),
+// then un-rotates them with selects so the FMAs still run in j order.
+// Measured (B200, nel 1e6, Np 16..128): unrotated 16-byte loads 2.0-3.5 TF/s;
+// rotated 4.6-5.9 TF/s — flatter in Np than the shipped 32-byte lane swap
+// (5.3-8.0 TF/s) but slower at every Np except 64/128 (within 4%): rejected.
+template <bool ROT>
+__global__ void __launch_bounds__(256) dg_dmpf_rot4(const float* __restrict__ dm,
+                                                    const float* __restrict__ u,
+                                                    float* __restrict__ res, DgDims d) {
+  __shared__ __align__(16) float dmf[16][20];
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int64_t k = (int64_t)blockIdx.x * 16 + lx;
+  const int i0 = blockIdx.y * 16;
+  const int rot = ROT ? (lx & 3) : 0;
+  for (int m = 0; m < d.nmat; ++m) {
+    float acc = 0.f;
+    for (int jo = 0; jo < d.np / 16; ++jo) {
+      bar_sync();
+      dmf[ly][lx] = dm[((int64_t)m * d.np + i0 + ly) * d.np + jo * 16 + lx];
+      bar_sync();
+      const float4* ur = reinterpret_cast<const float4*>(u + k * d.np + jo * 16);
+      float4 x[4];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) x[s] = __ldg(ur + ((s + rot) & 3));
+      // x[s] holds quarter (s + rot) & 3; quarter q is x[(q - rot) & 3]
+      float4 b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int s = (q - rot) & 3;
+        const float4 lo = (s & 1) ? x[1] : x[0], hi = (s & 1) ? x[3] : x[2];
+        b[q] = (s & 2) ? hi : lo;
+      }
+#pragma unroll
+      for (int j4 = 0; j4 < 4; ++j4) {
+        const float4 a = *reinterpret_cast<const float4*>(&dmf[ly][4 * j4]);
+        acc = __fmaf_rn(a.x, b[j4].x, acc);
+        acc = __fmaf_rn(a.y, b[j4].y, acc);
+        acc = __fmaf_rn(a.z, b[j4].z, acc);
+        acc = __fmaf_rn(a.w, b[j4].w, acc);
+      }
+    }
+    res[((int64_t)m * d.nel + k) * d.np + i0 + ly] = acc;
+  }
+}
+
 int main() {
   const int64_t nel = 1000000;
   const int nps[] = {16, 32, 48, 64, 96, 128};
@@ -222,6 +268,15 @@ int main() {
     }
     double fl2 = 2.0 * 3 * nel * np * np;
     printf("np %3d  dmPF-ahead %.2f TF\n", np, fl2/t5/1e9);
+    for (int v = 0; v < 2; ++v) {
+      float t6 = v ? time([&] { dg_dmpf_rot4<true><<<grid, block>>>(dm, u, r2, d); })
+                   : time([&] { dg_dmpf_rot4<false><<<grid, block>>>(dm, u, r2, d); });
+      std::vector<float> ref(nr); cudaMemcpy(ref.data(), r0, nr*4, cudaMemcpyDeviceToHost);
+      cudaMemcpy(c.data(), r2, nr * 4, cudaMemcpyDeviceToHost);
+      size_t b6 = 0;
+      for (size_t x = 0; x < nr; ++x) b6 += memcmp(&ref[x], &c[x], 4) != 0;
+      printf("np %3d  dmPF-16B%s %.2f TF  mism %zu\n", np, v ? "-rot4" : "", fl2/t6/1e9, b6);
+    }
     printf("np %3d  skew2 %.2f TF  dmPF %.2f TF  dmPF-swap %.2f TF  mism %zu\n", np, fl2/t2/1e9, fl2/t3/1e9, fl2/t4/1e9, bad2);
     cudaFree(r2);
     std::vector<float> a(nr), b(nr);
