@@ -8,7 +8,6 @@ is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
-import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent

@@ -7,7 +7,6 @@ symbolic counts and feature values, the reference interpreter outputs and the
 Levenberg-Marquardt fits are byte-identical to the reference's own output
 (tests/golden/reference.json). Skipped where /root/reference is absent
 (the GPU box)."""
-import os
 import subprocess
 from pathlib import Path
 
