@@ -40,6 +40,15 @@
 namespace ps {
 namespace {
 
+#ifndef DGTC_STAGES
+#define DGTC_STAGES 0
+#endif
+#ifndef DGTC_ORDER
+#define DGTC_ORDER 0
+#endif
+#ifndef DGTC_EPI
+#define DGTC_EPI 4
+#endif
 constexpr int BM = 128, BK = 32;    // element rows per tile; fp32 per 128-byte row
 constexpr int U_BLK = BM * BK * 4;  // 16 KB per K block of a u tile
 constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in dynamic shared memory
@@ -158,12 +167,24 @@ struct Cfg {
   // one (m, K block) of dm: NP rows x 128 B (a CTA pair: NP / 2 rows each)
   static constexpr int DM_ROWS = PAIR ? NP / 2 : NP;
   static constexpr int DM_BLK = DM_ROWS * 128;
-  // shared memory: the CTA's resident dm matrices + a u ring (8 stages at
-  // Np <= 32, whose tiles are short, else 4) + epilogue buffers per warp
-  // (4 warps x OUT_BUFS x 32 rows x 128 B) within 227 KB
-  static constexpr int STAGES = NP <= 32 ? 8 : 4;
-  static constexpr int OUT_BUFS = NP <= 32 ? 4 : 2;
-  static constexpr int OUT_BYTES = 4 * OUT_BUFS * 4096;
+  // shared memory: the CTA's resident dm matrices + a u ring + epilogue
+  // buffers per warp (4 warps x OUT_BUFS x 32 rows x 128 B) within 227 KB.
+  // Ring depth measured per Np (nel = 1e6, tools/exp/epi.sh): 8 stages at
+  // Np <= 32 (short tiles), 4 at 48-96 (6-8 cost 5-13% there), 6 at Np >= 112
+  // (one matrix per CTA: 5.4 -> 6.1 TB/s at Np = 128 against 4 stages).
+  // Build-time knobs for such sweeps: DGTC_STAGES, DGTC_EPI (8 epilogue warps:
+  // no gain), DGTC_ORDER (1 = blocked tile order: 2-8% slower everywhere).
+  static constexpr int STAGES = DGTC_STAGES ? DGTC_STAGES : NP <= 32 ? 8 : NP >= 112 ? 6 : 4;
+  // epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter,
+  // alternating chunks); each owns OUT_BUFS 4 KB staging buffers
+  static constexpr int EPI = DGTC_EPI;
+  static constexpr int FIXED3 = 3 * NKB * DM_BLK + STAGES * U_BLK + 1280;
+  static constexpr int FIXED = FIXED3 + EPI * 4096 <= 232448 ? FIXED3 : NKB * DM_BLK + STAGES * U_BLK + 1280;
+  static constexpr int FIT_BUFS = (232448 - FIXED) / (EPI * 4096);
+  static constexpr int OUT_BUFS =
+      EPI == 4 ? (NP <= 32 ? 4 : 2) : (FIT_BUFS >= 4 ? 4 : FIT_BUFS >= 2 ? 2 : 1);
+  static constexpr int OUT_BYTES = EPI * OUT_BUFS * 4096;
+  static constexpr int THREADS = 64 + 32 * EPI;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NP >> 3) << 17) |
                                     (uint32_t((PAIR ? 2 * BM : BM) >> 4) << 24);
   static int smem_bytes(int nmat) { return nmat * NKB * DM_BLK + STAGES * U_BLK + OUT_BYTES + 1024 + 256; }
@@ -174,7 +195,7 @@ struct Cfg {
 // the N-half (Np/2 rows) of every dm matrix, so at Np = 128 all three
 // matrices fit beside the u ring without the per-matrix groups.
 template <int NP, bool PAIR>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(64 + 32 * DGTC_EPI, 1)
     dg_tc_kernel(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmD,
                  const __grid_constant__ CUtensorMap tmR, int64_t nel, int nmat, int groups, int nacc,
                  uint32_t tmem_cols) {
@@ -200,6 +221,13 @@ __global__ void __launch_bounds__(192, 1)
   const int units = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
   const int grp = unit % groups, cta = unit / groups, ncta = units / groups;
   const int m0 = grp * nmat;
+#if DGTC_ORDER == 1
+  // blocked: CTA c owns tiles [c * per, (c + 1) * per)
+  const int64_t per = (ntiles + ncta - 1) / ncta;
+  const int64_t t_first = cta * per, t_end = t_first + per < ntiles ? t_first + per : ntiles, t_step = 1;
+#else
+  const int64_t t_first = cta, t_end = ntiles, t_step = ncta;  // round robin
+#endif
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + C::STAGES);
   const uint32_t tfull0 = smem_u32(bars + 2 * C::STAGES), tempty0 = tfull0 + 16;
   const uint32_t dm_full = tfull0 + 32;
@@ -212,7 +240,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
-      mbar_init(tempty0 + 8 * a, PAIR ? 256 : 128);  // pair: both CTAs' epilogues
+      mbar_init(tempty0 + 8 * a, (PAIR ? 64 : 32) * C::EPI);  // pair: both CTAs' epilogues
     }
     mbar_init(dm_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -252,7 +280,7 @@ __global__ void __launch_bounds__(192, 1)
             tma_2d(dst, &tmD, dm_full, kb * BK, row);
         }
       int it = 0;
-      for (int64_t t = cta; t < ntiles; t += ncta)
+      for (int64_t t = t_first; t < t_end; t += t_step)
         for (int kb = 0; kb < C::NKB; ++kb, ++it) {
           const int s = it % C::STAGES;
           if (it >= C::STAGES) mbar_wait(empty0 + 8 * s, ((it / C::STAGES) - 1) & 1);
@@ -270,7 +298,7 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0 && leader) {  // MMA issue (a pair: the leader, for both CTAs)
       mbar_wait(dm_full, 0);
       int it = 0, local = 0;
-      for (int64_t t = cta; t < ntiles; t += ncta, ++local) {
+      for (int64_t t = t_first; t < t_end; t += t_step, ++local) {
         const int a = local % nacc;
         const int use = local / nacc;  // how often accumulator a was used before
         if (use >= 1) mbar_wait(tempty0 + 8 * a, (use - 1) & 1);
@@ -299,9 +327,10 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {  // epilogue: warp w <-> TMEM lanes 32(w%4).. = element rows
-    const int q4 = warp & 3;
+    const int q4 = warp & 3, e = warp - 2;
+    const int half = e >> 2, nhalf = C::EPI / 4;  // 8 warps: chunk j to half j % 2
     int local = 0, nchunk = 0;
-    for (int64_t t = cta; t < ntiles; t += ncta, ++local) {
+    for (int64_t t = t_first; t < t_end; t += t_step, ++local) {
       const int a = local % nacc;
       mbar_wait(tfull0 + 8 * a, (local / nacc) & 1);
       __syncwarp();
@@ -311,9 +340,11 @@ __global__ void __launch_bounds__(192, 1)
       // (128-byte swizzle: 16-B chunk q of row l at q ^ (l & 7), conflict-free)
       // -> one TMA bulk store of 32 rows x 32 columns; rows past nel and
       // columns past Np fall outside the tensor map and are clipped
-      const uint32_t ob0 = smem_u32(sout + q4 * C::OUT_BUFS * 4096);
+      const uint32_t ob0 = smem_u32(sout + e * C::OUT_BUFS * 4096);
+      int cj = 0;
       for (int m = 0; m < nmat; ++m)
-        for (int c = 0; c < NP; c += 32, ++nchunk) {
+        for (int c = 0; c < NP; c += 32) {
+          if (nhalf > 1 && (cj++ % nhalf) != half) continue;
           const uint32_t ob = ob0 + uint32_t(nchunk % C::OUT_BUFS) * 4096;
           if (nchunk >= C::OUT_BUFS) {  // the store that last read this buffer is done
             if (lane == 0) {
@@ -350,6 +381,7 @@ __global__ void __launch_bounds__(192, 1)
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
+          ++nchunk;
         }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       if constexpr (PAIR)
@@ -455,7 +487,7 @@ int launch_cfg(Ctx* c, const ps_kernel_desc* d) {
   if constexpr (PAIR) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * units);
-    cfg.blockDim = dim3(192);
+    cfg.blockDim = dim3(C::THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c->stream;
     cudaLaunchAttribute at[1];
@@ -468,7 +500,7 @@ int launch_cfg(Ctx* c, const ps_kernel_desc* d) {
     const cudaError_t e = cudaLaunchKernelEx(&cfg, dg_tc_kernel<NP, true>, tu, td, tr, d->nel, nmat, groups, nacc, tcols);
     if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "dg_diff_tc pair launch: %s", cudaGetErrorString(e));
   } else {
-    dg_tc_kernel<NP, false><<<units, 192, smem, c->stream>>>(tu, td, tr, d->nel, nmat, groups, nacc, tcols);
+    dg_tc_kernel<NP, false><<<units, C::THREADS, smem, c->stream>>>(tu, td, tr, d->nel, nmat, groups, nacc, tcols);
   }
   return PS_OK;
 }
