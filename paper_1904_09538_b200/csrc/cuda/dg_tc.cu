@@ -40,6 +40,9 @@
 namespace ps {
 namespace {
 
+#ifndef DGTC_CPS
+#define DGTC_CPS 1
+#endif
 #ifndef DGTC_STAGES
 #define DGTC_STAGES 0
 #endif
@@ -173,8 +176,11 @@ struct Cfg {
   // Np <= 32 (short tiles), 4 at 48-96 (6-8 cost 5-13% there), 6 at Np >= 112
   // (one matrix per CTA: 5.4 -> 6.1 TB/s at Np = 128 against 4 stages).
   // Build-time knobs for such sweeps: DGTC_STAGES, DGTC_EPI (8 epilogue warps:
-  // no gain), DGTC_ORDER (1 = blocked tile order: 2-8% slower everywhere).
-  static constexpr int STAGES = DGTC_STAGES ? DGTC_STAGES : NP <= 32 ? 8 : NP >= 112 ? 6 : 4;
+  // no gain), DGTC_ORDER (1 = blocked tile order: 2-8% slower everywhere),
+  // DGTC_CPS (2 = two CTAs per SM at Np <= 32: within noise).
+  // CTAs per SM: two at Np <= 32 when DGTC_CPS == 2 (smaller ring and buffers)
+  static constexpr int CPS = (DGTC_CPS == 2 && NP <= 32 && !PAIR) ? 2 : 1;
+  static constexpr int STAGES = DGTC_STAGES ? DGTC_STAGES : CPS == 2 ? 4 : NP <= 32 ? 8 : NP >= 112 ? 6 : 4;
   // epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter,
   // alternating chunks); each owns OUT_BUFS 4 KB staging buffers
   static constexpr int EPI = DGTC_EPI;
@@ -182,7 +188,7 @@ struct Cfg {
   static constexpr int FIXED = FIXED3 + EPI * 4096 <= 232448 ? FIXED3 : NKB * DM_BLK + STAGES * U_BLK + 1280;
   static constexpr int FIT_BUFS = (232448 - FIXED) / (EPI * 4096);
   static constexpr int OUT_BUFS =
-      EPI == 4 ? (NP <= 32 ? 4 : 2) : (FIT_BUFS >= 4 ? 4 : FIT_BUFS >= 2 ? 2 : 1);
+      EPI == 4 ? (NP <= 32 && CPS == 1 ? 4 : 2) : (FIT_BUFS >= 4 ? 4 : FIT_BUFS >= 2 ? 2 : 1);
   static constexpr int OUT_BYTES = EPI * OUT_BUFS * 4096;
   static constexpr int THREADS = 64 + 32 * EPI;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NP >> 3) << 17) |
@@ -481,7 +487,7 @@ int launch_cfg(Ctx* c, const ps_kernel_desc* d) {
   rc = make_res_map(&tr, c->out[0].ptr, d->nel, NP, nmat_all);
   if (rc) return rc;
   const int64_t ntiles = (d->nel + (PAIR ? 2 * BM : BM) - 1) / (PAIR ? 2 * BM : BM);
-  const int units_max = PAIR ? c->sm_count / 2 : c->sm_count;  // CTAs, or pairs
+  const int units_max = PAIR ? c->sm_count / 2 : c->sm_count * C::CPS;  // CTAs, or pairs
   const int64_t per_group = std::min<int64_t>(ntiles, std::max(1, units_max / groups));
   const int units = (int)(per_group * groups);
   if constexpr (PAIR) {
