@@ -41,8 +41,8 @@ if [ "$only" = "model" ] || [ -z "$only" ]; then
   done
 fi
 if [ -z "$only" ] || [ "$only" = "launches" ]; then
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
-  --log-file $out/launches_all.csv python bench.py --steps 1 --warmup 1 --trials-per-step 1 \
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 8000 --csv \
+  --log-file $out/launches_all.csv python bench.py --steps 1 --warmup 3 --trials-per-step 1 \
   --c5-points 100000 --tc 0 > $out/launches_bench.log 2>&1
 echo "launches rc=$?"
 fi
