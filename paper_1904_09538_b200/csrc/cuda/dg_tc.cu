@@ -40,6 +40,9 @@
 namespace ps {
 namespace {
 
+#ifndef DGTC_SUB_MASK  // bit NP/16 - 1: two 128-row sub-tiles per tile at that Np
+#define DGTC_SUB_MASK 8  // Np = 64 (5.4-5.5 -> 5.9-6.0 TB/s; no gain at 16/32, -9% at 48)
+#endif
 #ifndef DGTC_CPS
 #define DGTC_CPS 1
 #endif
@@ -177,15 +180,20 @@ struct Cfg {
   // (one matrix per CTA: 5.4 -> 6.1 TB/s at Np = 128 against 4 stages).
   // Build-time knobs for such sweeps: DGTC_STAGES, DGTC_EPI (8 epilogue warps:
   // no gain), DGTC_ORDER (1 = blocked tile order: 2-8% slower everywhere),
-  // DGTC_CPS (2 = two CTAs per SM at Np <= 32: within noise).
+  // DGTC_CPS (2 = two CTAs per SM at Np <= 32: within noise), DGTC_SUB_MASK
+  // (256-row tiles as two M = 128 sub-tiles; on at Np = 64 only).
   // CTAs per SM: two at Np <= 32 when DGTC_CPS == 2 (smaller ring and buffers)
   static constexpr int CPS = (DGTC_CPS == 2 && NP <= 32 && !PAIR) ? 2 : 1;
-  static constexpr int STAGES = DGTC_STAGES ? DGTC_STAGES : CPS == 2 ? 4 : NP <= 32 ? 8 : NP >= 112 ? 6 : 4;
+  // SUB 128-row sub-tiles per tile (2: half as many tiles, each twice as large)
+  static constexpr int SUB = (!PAIR && ((DGTC_SUB_MASK >> (NP / 16 - 1)) & 1)) ? 2 : 1;
+  static constexpr int SBLK = U_BLK * SUB;  // bytes per ring stage
+  static constexpr int STAGES = DGTC_STAGES ? DGTC_STAGES
+                                : (CPS == 2 || SUB == 2) ? 4 : NP <= 32 ? 8 : NP >= 112 ? 6 : 4;
   // epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter,
   // alternating chunks); each owns OUT_BUFS 4 KB staging buffers
   static constexpr int EPI = DGTC_EPI;
-  static constexpr int FIXED3 = 3 * NKB * DM_BLK + STAGES * U_BLK + 1280;
-  static constexpr int FIXED = FIXED3 + EPI * 4096 <= 232448 ? FIXED3 : NKB * DM_BLK + STAGES * U_BLK + 1280;
+  static constexpr int FIXED3 = 3 * NKB * DM_BLK + STAGES * SBLK + 1280;
+  static constexpr int FIXED = FIXED3 + EPI * 4096 <= 232448 ? FIXED3 : NKB * DM_BLK + STAGES * SBLK + 1280;
   static constexpr int FIT_BUFS = (232448 - FIXED) / (EPI * 4096);
   static constexpr int OUT_BUFS =
       EPI == 4 ? (NP <= 32 && CPS == 1 ? 4 : 2) : (FIT_BUFS >= 4 ? 4 : FIT_BUFS >= 2 ? 2 : 1);
@@ -193,7 +201,7 @@ struct Cfg {
   static constexpr int THREADS = 64 + 32 * EPI;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NP >> 3) << 17) |
                                     (uint32_t((PAIR ? 2 * BM : BM) >> 4) << 24);
-  static int smem_bytes(int nmat) { return nmat * NKB * DM_BLK + STAGES * U_BLK + OUT_BYTES + 1024 + 256; }
+  static int smem_bytes(int nmat) { return nmat * NKB * DM_BLK + STAGES * SBLK + OUT_BYTES + 1024 + 256; }
 };
 
 // PAIR: a cluster of two CTAs (cta_group::2) computes 256-row tiles with
@@ -215,11 +223,11 @@ __global__ void __launch_bounds__(64 + 32 * DGTC_EPI, 1)
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sdm = smem;                                  // [m][kb] blocks of NP x 128 B
   uint8_t* su = smem + nmat * C::NKB * C::DM_BLK;       // STAGES x (128 x 128 B)
-  uint8_t* sout = su + C::STAGES * U_BLK;                // [warp][OUT_BUFS] x (32 x 128 B)
+  uint8_t* sout = su + C::STAGES * C::SBLK;               // [warp][OUT_BUFS] x (32 x 128 B)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sout + C::OUT_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 5);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int TROWS = PAIR ? 2 * BM : BM;  // element rows per tile (per pair)
+  constexpr int TROWS = PAIR ? 2 * BM : BM * C::SUB;  // element rows per tile (per pair)
   const int64_t ntiles = (nel + TROWS - 1) / TROWS;
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
   const bool leader = rank == 0;
@@ -237,7 +245,7 @@ __global__ void __launch_bounds__(64 + 32 * DGTC_EPI, 1)
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + C::STAGES);
   const uint32_t tfull0 = smem_u32(bars + 2 * C::STAGES), tempty0 = tfull0 + 16;
   const uint32_t dm_full = tfull0 + 32;
-  const uint32_t acc_cols = uint32_t(nmat * NP);
+  const uint32_t acc_cols = uint32_t(C::SUB * nmat * NP);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -295,8 +303,8 @@ __global__ void __launch_bounds__(64 + 32 * DGTC_EPI, 1)
             if (leader) mbar_expect_tx(full0 + 8 * s, 2 * U_BLK);
             tma2_2d(smem_u32(su + s * U_BLK), &tmU, full0 + 8 * s, kb * BK, row);
           } else {
-            mbar_expect_tx(full0 + 8 * s, U_BLK);
-            tma_2d(smem_u32(su + s * U_BLK), &tmU, full0 + 8 * s, kb * BK, row);
+            mbar_expect_tx(full0 + 8 * s, C::SBLK);
+            tma_2d(smem_u32(su + s * C::SBLK), &tmU, full0 + 8 * s, kb * BK, row);
           }
         }
     }
@@ -314,17 +322,19 @@ __global__ void __launch_bounds__(64 + 32 * DGTC_EPI, 1)
           const int s = it % C::STAGES;
           mbar_wait(full0 + 8 * s, (it / C::STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t ub = smem_u32(su + s * U_BLK);
+          const uint32_t ub0 = smem_u32(su + s * C::SBLK);
           const int nks = (NP - kb * BK) >= BK ? BK / 8 : (NP - kb * BK) / 8;
-          for (int m = 0; m < nmat; ++m) {
-            const uint32_t db = smem_u32(sdm + (m * C::NKB + kb) * C::DM_BLK);
-            for (int ks = 0; ks < nks; ++ks) {
-              if constexpr (PAIR)
-                mma2_tf32(d0 + uint32_t(m * NP), desc_kmajor(ub + ks * 32), desc_kmajor(db + ks * 32), C::IDESC,
-                          (kb | ks) != 0);
-              else
-                mma_tf32(d0 + uint32_t(m * NP), desc_kmajor(ub + ks * 32), desc_kmajor(db + ks * 32), C::IDESC,
-                         (kb | ks) != 0);
+          for (int h = 0; h < C::SUB; ++h) {  // sub-tile h: u rows h*128.., accumulator block h
+            const uint32_t ub = ub0 + uint32_t(h * U_BLK);
+            for (int m = 0; m < nmat; ++m) {
+              const uint32_t db = smem_u32(sdm + (m * C::NKB + kb) * C::DM_BLK);
+              const uint32_t dc = d0 + uint32_t((h * nmat + m) * NP);
+              for (int ks = 0; ks < nks; ++ks) {
+                if constexpr (PAIR)
+                  mma2_tf32(dc, desc_kmajor(ub + ks * 32), desc_kmajor(db + ks * 32), C::IDESC, (kb | ks) != 0);
+                else
+                  mma_tf32(dc, desc_kmajor(ub + ks * 32), desc_kmajor(db + ks * 32), C::IDESC, (kb | ks) != 0);
+              }
             }
           }
           if constexpr (PAIR) commit2(empty0 + 8 * s); else mma_commit(empty0 + 8 * s);
@@ -348,8 +358,10 @@ __global__ void __launch_bounds__(64 + 32 * DGTC_EPI, 1)
       // columns past Np fall outside the tensor map and are clipped
       const uint32_t ob0 = smem_u32(sout + e * C::OUT_BUFS * 4096);
       int cj = 0;
-      for (int m = 0; m < nmat; ++m)
+      for (int sb = 0; sb < C::SUB; ++sb)  // (sub-tile, matrix) = accumulator block sm
+        for (int m = 0; m < nmat; ++m)
         for (int c = 0; c < NP; c += 32) {
+          const int sm = sb * nmat + m;
           if (nhalf > 1 && (cj++ % nhalf) != half) continue;
           const uint32_t ob = ob0 + uint32_t(nchunk % C::OUT_BUFS) * 4096;
           if (nchunk >= C::OUT_BUFS) {  // the store that last read this buffer is done
@@ -365,10 +377,10 @@ __global__ void __launch_bounds__(64 + 32 * DGTC_EPI, 1)
           }
           uint32_t v[32];
           if (c + 32 <= NP) {
-            tmem_ld<32>(tb + uint32_t(m * NP + c), v);
+            tmem_ld<32>(tb + uint32_t(sm * NP + c), v);
           } else {
             uint32_t(&h)[16] = *reinterpret_cast<uint32_t(*)[16]>(v);
-            tmem_ld<16>(tb + uint32_t(m * NP + c), h);
+            tmem_ld<16>(tb + uint32_t(sm * NP + c), h);
           }
 #pragma unroll
           for (int q = 0; q < 8; ++q)
@@ -383,7 +395,7 @@ __global__ void __launch_bounds__(64 + 32 * DGTC_EPI, 1)
             asm volatile(
                 "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                     reinterpret_cast<uint64_t>(&tmR)),
-                "r"(c), "r"(int(t * TROWS) + int(rank) * BM + 32 * q4), "r"(m0 + m), "r"(ob)
+                "r"(c), "r"(int(t * TROWS) + int(rank) * BM + sb * BM + 32 * q4), "r"(m0 + m), "r"(ob)
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
@@ -475,18 +487,19 @@ int launch_cfg(Ctx* c, const ps_kernel_desc* d) {
   std::call_once(attr, [] {
     cudaFuncSetAttribute(dg_tc_kernel<NP, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
   });
-  const int cols = nmat * NP;
+  const int cols = C::SUB * nmat * NP;
   const int nacc = 2 * cols <= 512 ? 2 : 1;
   uint32_t tcols = 32;
   while (tcols < uint32_t(nacc * cols)) tcols <<= 1;
   CUtensorMap tu, td, tr;
-  int rc = make_map(&tu, c->in[1].ptr, d->nel, NP, BM);
+  int rc = make_map(&tu, c->in[1].ptr, d->nel, NP, BM * C::SUB);
   if (rc) return rc;
   rc = make_map(&td, c->in[0].ptr, (int64_t)nmat_all * NP, NP, C::DM_ROWS);
   if (rc) return rc;
   rc = make_res_map(&tr, c->out[0].ptr, d->nel, NP, nmat_all);
   if (rc) return rc;
-  const int64_t ntiles = (d->nel + (PAIR ? 2 * BM : BM) - 1) / (PAIR ? 2 * BM : BM);
+  const int trows = PAIR ? 2 * BM : BM * C::SUB;
+  const int64_t ntiles = (d->nel + trows - 1) / trows;
   const int units_max = PAIR ? c->sm_count / 2 : c->sm_count * C::CPS;  // CTAs, or pairs
   const int64_t per_group = std::min<int64_t>(ntiles, std::max(1, units_max / groups));
   const int units = (int)(per_group * groups);
