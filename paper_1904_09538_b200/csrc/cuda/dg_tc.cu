@@ -52,6 +52,9 @@ namespace {
 #ifndef DGTC_ORDER
 #define DGTC_ORDER 0
 #endif
+#ifndef DGTC_EPI8_MASK  // bit NP/16 - 1: 8 epilogue warps at that Np
+#define DGTC_EPI8_MASK 1  // Np = 16, whose short tiles are epilogue-latency bound: +4%
+#endif
 #ifndef DGTC_EPI
 #define DGTC_EPI 4
 #endif
@@ -178,8 +181,8 @@ struct Cfg {
   // Ring depth measured per Np (nel = 1e6, tools/exp/epi.sh): 8 stages at
   // Np <= 32 (short tiles), 4 at 48-96 (6-8 cost 5-13% there), 6 at Np >= 112
   // (one matrix per CTA: 5.4 -> 6.1 TB/s at Np = 128 against 4 stages).
-  // Build-time knobs for such sweeps: DGTC_STAGES, DGTC_EPI (8 epilogue warps:
-  // no gain), DGTC_ORDER (1 = blocked tile order: 2-8% slower everywhere),
+  // Build-time knobs for such sweeps: DGTC_STAGES, DGTC_EPI / DGTC_EPI8_MASK
+  // (8 epilogue warps: +4% at Np = 16, none at 32, losses at 48/96), DGTC_ORDER (1 = blocked tile order: 2-8% slower everywhere),
   // DGTC_CPS (2 = two CTAs per SM at Np <= 32: within noise), DGTC_SUB_MASK
   // (256-row tiles as two M = 128 sub-tiles; on at Np = 64 only).
   // CTAs per SM: two at Np <= 32 when DGTC_CPS == 2 (smaller ring and buffers)
@@ -191,7 +194,7 @@ struct Cfg {
                                 : (CPS == 2 || SUB == 2) ? 4 : NP <= 32 ? 8 : NP >= 112 ? 6 : 4;
   // epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter,
   // alternating chunks); each owns OUT_BUFS 4 KB staging buffers
-  static constexpr int EPI = DGTC_EPI;
+  static constexpr int EPI = ((DGTC_EPI8_MASK >> (NP / 16 - 1)) & 1) ? 8 : DGTC_EPI;
   static constexpr int FIXED3 = 3 * NKB * DM_BLK + STAGES * SBLK + 1280;
   static constexpr int FIXED = FIXED3 + EPI * 4096 <= 232448 ? FIXED3 : NKB * DM_BLK + STAGES * SBLK + 1280;
   static constexpr int FIT_BUFS = (232448 - FIXED) / (EPI * 4096);
@@ -209,7 +212,7 @@ struct Cfg {
 // the N-half (Np/2 rows) of every dm matrix, so at Np = 128 all three
 // matrices fit beside the u ring without the per-matrix groups.
 template <int NP, bool PAIR>
-__global__ void __launch_bounds__(64 + 32 * DGTC_EPI, 1)
+__global__ void __launch_bounds__(Cfg<NP, PAIR>::THREADS, 1)
     dg_tc_kernel(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmD,
                  const __grid_constant__ CUtensorMap tmR, int64_t nel, int nmat, int groups, int nacc,
                  uint32_t tmem_cols) {
