@@ -22,6 +22,9 @@ cap dg_dmpf_1e6 dg_dmpf "dg_diff__dtype-float32__nelements-1000000__nmatrices-3_
 cap dg_dmpft_1e6 dg_dmpf "dg_diff__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-64__variant-dmPFtrans"
 cap dg_tc_64 dg_tc_kernel "dg_diff_tc__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-64"
 cap dg_tc_48 dg_tc_kernel "dg_diff_tc__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-48"
+cap dg_tc_32 dg_tc_kernel "dg_diff_tc__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-32"
+cap dg_tc_16 dg_tc_kernel "dg_diff_tc__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-16"
+cap dg_tc_128 dg_tc_kernel "dg_diff_tc__dtype-float32__nelements-1000000__nmatrices-3__nunit_nodes-128"
 cap madd flops_pattern "flops_madd_pattern__dtype-float32__lid_stride_0-1__lid_stride_1-2048__lsize_0-16__lsize_1-16__m-128__nelements-2097152"
 cap tc_8192 matmul_tc "matmul_sq_tc__dtype-float32__lsize_0-16__lsize_1-16__n-8192"
 cap gmem2 gmem_pattern "gmem_pattern__dtype-float32__lid_stride_0-1__lid_stride_1-2048__lsize_0-16__lsize_1-16__n_input_arrays-2__nelements-671088640"
