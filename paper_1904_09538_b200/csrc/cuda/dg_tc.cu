@@ -53,7 +53,7 @@ namespace {
 #define DGTC_ORDER 0
 #endif
 #ifndef DGTC_EPI8_MASK  // bit NP/16 - 1: 8 epilogue warps at that Np
-#define DGTC_EPI8_MASK 1  // Np = 16, whose short tiles are epilogue-latency bound: +4%
+#define DGTC_EPI8_MASK 3  // Np = 16 (+4%) and 32 (with a 3-stage ring: +5%), short tiles
 #endif
 #ifndef DGTC_EPI
 #define DGTC_EPI 4
@@ -179,7 +179,8 @@ struct Cfg {
   // shared memory: the CTA's resident dm matrices + a u ring + epilogue
   // buffers per warp (4 warps x OUT_BUFS x 32 rows x 128 B) within 227 KB.
   // Ring depth measured per Np (nel = 1e6, tools/exp/epi.sh): 8 stages at
-  // Np <= 32 (short tiles), 4 at 48-96 (6-8 cost 5-13% there), 6 at Np >= 112
+  // Np = 16, 3 at Np = 32 (with 8 epilogue warps and 4 output buffers each),
+  // 4 at 48-96 (6-8 cost 5-13% there), 6 at Np >= 112
   // (one matrix per CTA: 5.4 -> 6.1 TB/s at Np = 128 against 4 stages).
   // Build-time knobs for such sweeps: DGTC_STAGES, DGTC_EPI / DGTC_EPI8_MASK
   // (8 epilogue warps: +4% at Np = 16, none at 32, losses at 48/96), DGTC_ORDER (1 = blocked tile order: 2-8% slower everywhere),
@@ -191,7 +192,7 @@ struct Cfg {
   static constexpr int SUB = (!PAIR && ((DGTC_SUB_MASK >> (NP / 16 - 1)) & 1)) ? 2 : 1;
   static constexpr int SBLK = U_BLK * SUB;  // bytes per ring stage
   static constexpr int STAGES = DGTC_STAGES ? DGTC_STAGES
-                                : (CPS == 2 || SUB == 2) ? 4 : NP <= 32 ? 8 : NP >= 112 ? 6 : 4;
+                                : (CPS == 2 || SUB == 2) ? 4 : NP <= 16 ? 8 : NP <= 32 ? 3 : NP >= 112 ? 6 : 4;
   // epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter,
   // alternating chunks); each owns OUT_BUFS 4 KB staging buffers
   static constexpr int EPI = ((DGTC_EPI8_MASK >> (NP / 16 - 1)) & 1) ? 8 : DGTC_EPI;
@@ -369,12 +370,7 @@ __global__ void __launch_bounds__(Cfg<NP, PAIR>::THREADS, 1)
           const uint32_t ob = ob0 + uint32_t(nchunk % C::OUT_BUFS) * 4096;
           if (nchunk >= C::OUT_BUFS) {  // the store that last read this buffer is done
             if (lane == 0) {
-              if constexpr (C::OUT_BUFS == 4)
-                asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
-              else if constexpr (C::OUT_BUFS == 2)
-                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-              else
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::OUT_BUFS - 1) : "memory");
             }
             __syncwarp();
           }
