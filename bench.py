@@ -35,6 +35,7 @@ sys.path.insert(0, str(ROOT))
 import numpy as np  # noqa: E402
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+METRIC = "suite GB/s"
 
 
 def peaks() -> tuple[dict, str]:
@@ -69,6 +70,10 @@ class Dist:
             dist.init_process_group(backend=backend)
             self.pg = dist
             self.backend = backend
+            # communicator init, for the driver's rank-count check
+            print(f"[bench] rank {self.rank}: {backend} process group initialised, "
+                  f"nranks {dist.get_world_size()}, device {self.device}", file=sys.stderr,
+                  flush=True)
 
     def barrier(self):
         if self.pg:
@@ -558,7 +563,15 @@ def c5_report(dev, parts, variants: list[dict], npts: int = 1_000_000, dist=None
     t = PredictionTables(variants)
     pts = c5_points(npts)
     lo, hi = c5_block(npts, rank, world)
-    t.eval_gpu(dev, pts[lo:lo + max(1, min(4096, hi - lo))])  # warm
+    err = None
+    try:
+        t.eval_gpu(dev, pts[lo:lo + max(1, min(4096, hi - lo))])  # warm
+    except Exception as e:  # every rank learns of it before the collectives
+        err = e
+    if dist and dist.max(float(err is not None)) > 0:
+        raise RuntimeError(f"C5 evaluation failed on a rank: {err}")
+    if err is not None:
+        raise err
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
@@ -633,46 +646,36 @@ def reference_model_sample(seconds: float = 2.0) -> dict:
     return json.loads(r.stdout)
 
 
-def cpu_gmem_sample(elements: int = 1 << 26, reps: int = 3) -> dict:
-    from oracle import suite as oracle_suite
-    from paper_1904_09538_b200 import desc_from_id, kernel_io
-    vid = ("gmem_pattern__dtype-float32__lid_stride_0-1__lid_stride_1-2048__lsize_0-16"
-           f"__lsize_1-16__n_input_arrays-2__nelements-{elements}")
-    d = desc_from_id(vid)
-    io = kernel_io(d)
-    ins = [np.ones(elements, np.float32), np.ones(elements, np.float32)]
-    oracle_suite.run(d, io, ins)  # warm
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        oracle_suite.run(d, io, ins)
-    dt = (time.perf_counter() - t0) / reps
-    return {"value": round(io.bytes_global / dt / 1e9, 2), "unit": "GB/s",
-            "cores": oracle_suite.threads(), "kind": "port",
-            "sample": f"gmem_pattern k=2 restatement (oracle/suite_ref.c, OpenMP) on "
-                      f"E=2^{int(math.log2(elements))} fp32, {reps} reps"}
+WORKLOAD_FILE = ROOT / "tests" / "golden" / "workload_{}.json"
 
 
-def run_reference_arm(args, dist: Dist) -> None:
-    """bench.py --impl reference: the reference path has no GPU code (SPEC.md:16,
-    597); its CPU implementation of this path is timed on the host cores — the
-    kernel restatement (oracle/suite_ref.c) over a bounded sample of the same
-    workload, plus the reference library's own feature/fit pipeline when
-    oracle/_ref was built."""
-    if dist.rank != 0:
-        return
-    from oracle import suite as oracle_suite
-    if dist.world > 1:
-        # torchrun pins OMP_NUM_THREADS=1 per rank; rank 0 runs the reference
-        # alone here, with every host thread
-        oracle_suite.set_threads(os.cpu_count() or 1)
-    from paper_1904_09538_b200 import desc_from_id, kernel_io
-    _, kernels = workload_kernels(args.workload)
+def workload_doc(name: str) -> dict:
+    """The workload's kernel ids as committed by tools/gen_workload_list.py
+    (the B200 catalog's expansion; tests/test_variants_cpu.py keeps it
+    current). Lets the reference arm run the same workload without loading
+    the product library."""
+    return json.loads(Path(str(WORKLOAD_FILE).format(name)).read_text())
+
+
+def bench_config(workload: str, n_kernels: int, n_cal: int, n_app: int, trials: int,
+                 world: int) -> dict:
+    """The `config` object of BOTH arms' lines (the driver compares them)."""
+    return {"workload": workload, "kernels": n_kernels, "calibration_kernels": n_cal,
+            "application_kernels": n_app, "trials_per_kernel": trials,
+            "l2": "no flush; HBM microbenchmarks use >= 1 GiB arrays (> 126 MB L2); trials of a "
+                  "kernel back to back as measure_kernel runs them (executor.cpp:40-48)",
+            "parallelism": f"(kernel, trial) units LPT-sharded over {world} rank(s)"}
+
+
+def reference_sample(kernels: list[str]) -> list:
+    """Bounded CPU sample of a workload for the oracle restatement: every
+    kernel except the cubic-cost ones above n = 1024 and DG above 10^5
+    elements, with the HBM arrays shrunk to 2^24 elements (still larger than
+    the host LLC). Descriptors come from oracle/variants.py, not the product."""
+    from oracle import variants
     sample = []
     for vid in kernels:
-        d = desc_from_id(vid)
-        io = kernel_io(d)
-        # bound the sample: skip the cubic-cost kernels above n = 1024 and shrink
-        # HBM arrays to 2^24 elements (still larger than the host LLC)
+        d = variants.parse(vid)
         if d.gen in (7, 8) and d.n > 1024:
             continue
         if d.gen in (1, 6) and d.nelements > (1 << 24):
@@ -681,40 +684,68 @@ def run_reference_arm(args, dist: Dist) -> None:
             continue
         if d.gen in (11, 12) and d.nel > 100000:
             continue
-        sample.append((vid, d, io))
-    # add the HBM microbenchmarks at a bounded size
+        sample.append((vid, d, variants.io_of(d)))
     for k in (1, 2):
         vid = ("gmem_pattern__dtype-float32__lid_stride_0-1__lid_stride_1-2048__lsize_0-16"
                f"__lsize_1-16__n_input_arrays-{k}__nelements-{1 << 24}")
-        d = desc_from_id(vid)
-        sample.append((vid, d, kernel_io(d)))
+        d = variants.parse(vid)
+        sample.append((vid, d, variants.io_of(d)))
+    return sample
+
+
+def time_reference_sample(sample: list, warmup: int, steps: int, threads: int | None = None):
+    """oracle/suite_ref.c (OpenMP) over the sample: (GB/s, seconds, cores)."""
+    from oracle import suite as oracle_suite
+    if threads:
+        oracle_suite.set_threads(threads)
     rng = np.random.default_rng(0)
     inputs = {}
     for vid, d, io in sample:
         dt = np.float32 if io.elem_bytes == 4 else np.float64
-        inputs[vid] = [rng.random(io.input_elems[i]).astype(dt) for i in range(io.n_inputs)]
-    for _ in range(args.warmup):
+        inputs[vid] = [rng.random(n).astype(dt) for n in io.input_elems]
+    for _ in range(warmup):
         for vid, d, io in sample:
             oracle_suite.run(d, io, inputs[vid])
     t0 = time.perf_counter()
-    bytes_total = 0.0
-    for _ in range(args.steps):
+    nbytes = 0.0
+    for _ in range(steps):
         for vid, d, io in sample:
             oracle_suite.run(d, io, inputs[vid])
-            bytes_total += io.bytes_global
+            nbytes += io.bytes_global
     dt = time.perf_counter() - t0
-    value = bytes_total / dt / 1e9
+    return nbytes / dt / 1e9, dt, oracle_suite.threads()
+
+
+def sample_note(sample: list, workload: str) -> str:
+    return (f"{len(sample)} kernels of the {workload} workload (matmul n<=1024, DG nel<=1e5, "
+            "HBM arrays 2^24) through oracle/suite_ref.c, OpenMP")
+
+
+def run_reference_arm(args, dist: Dist) -> None:
+    """bench.py --impl reference: the reference has no GPU code (SPEC.md:16,
+    597); its CPU implementation of this path is timed on the host cores — the
+    kernel restatement (oracle/suite_ref.c) over a bounded sample of the SAME
+    workload, same config/metric/unit as our arm. Never loads the product
+    library: ids come from the committed workload file, descriptors from
+    oracle/variants.py."""
+    if dist.rank != 0:
+        return
+    doc = workload_doc(args.workload)
+    kernels = doc["kernels"]
+    apps = {k for a in doc["applications"].values() for k in a["application"]}
+    sample = reference_sample(kernels)
+    value, dt, cores = time_reference_sample(sample, args.warmup, args.steps,
+                                             threads=os.cpu_count() or 1)
     line = {
-        "impl": "reference", "metric": "suite GB/s", "value": round(value, 3), "unit": "GB/s",
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: bounded CPU sample ({len(sample)} kernels)"},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": oracle_suite.threads(),
-                         "kind": "port",
-                         "sample": f"{len(sample)} suite kernels of the {args.workload} workload "
-                                   "(matmul n<=1024, DG nel<=1e5, HBM arrays 2^24) through "
-                                   "oracle/suite_ref.c"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (deterministic seed pattern, tests/support.hpp:35-44)",
+        "config": bench_config(args.workload, len(kernels), len(kernels) - len(apps), len(apps),
+                               args.steps * args.trials_per_step, args.gpus),
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores,
+                         "kind": "port", "sample": sample_note(sample, args.workload)},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -808,9 +839,12 @@ def run_ours(args, dist: Dist) -> None:
                   for i in e2e_set for j in range(ios[i].n_inputs))
     need_out = sum(int(ios[i].output_elems[j]) * ios[i].elem_bytes
                    for i in e2e_set for j in range(ios[i].n_outputs))
-    if need_in > pin_budget:
+    # every rank leaves together: a rank that cannot pin its inputs must not
+    # strand the others in the next collective
+    if dist.max(float(need_in > pin_budget)) > 0:
         raise SystemExit(f"rank {dist.rank}: e2e inputs need {need_in / 1e9:.1f} GB pinned host "
-                         f"memory, {pin_budget / 1e9:.1f} GB available to this rank")
+                         f"memory, {pin_budget / 1e9:.1f} GB available to this rank "
+                         "(or another rank's share was exceeded)")
     full_outputs = need_in + need_out <= pin_budget
     pinned = {}
     h2d = d2h = 0
@@ -1009,68 +1043,80 @@ def run_ours(args, dist: Dist) -> None:
             tensor_variant["dg_diff_tc"] = dg_tensor_variant_report(dev, mean_s)
     except Exception as e:
         tensor_variant = {"error": str(e)}
-    n_app = sum(len(app) for _, _, app in parts)
-    n_cal = len(kernels) - len({k for _, _, app in parts for k in app})
+    n_app = len({k for _, _, app in parts for k in app})
+    n_cal = len(kernels) - n_app
+    e2e_launch_total = int(len(table) + args.steps * e2e_launches)
+    cpu = None
+    if dist.world == 1:
+        # the oracle restatement on the host cores: the reference arm's
+        # bounded sample of this workload, 1 warm-up + 2 passes
+        sample = reference_sample(kernels)
+        v, _dt, cores = time_reference_sample(sample, 1, 2, threads=os.cpu_count() or 1)
+        cpu = {"value": round(v, 3), "unit": "GB/s", "cores": cores, "kind": "port",
+               "sample": sample_note(sample, args.workload)}
+    ref_lib = reference_model_sample() if dist.world == 1 else None
+    detail = {
+        "models": models, "headline": heads, "model_eval": model_eval,
+        "overlap_diagnosis": diagnosis, "tensor_variant": tensor_variant,
+        "roofline": roofline, "roofline_hbm": roofline_hbm, "suite_rooflines": suite_rooflines,
+        "suite_hbm_GBps": round(hbm_b / hbm_t / 1e9, 1) if hbm_t else None,
+        "suite_flops_TFps": round(fl / fl_t / 1e12, 2) if fl_t else None,
+        "cpu_baseline_reference": ref_lib,
+        "e2e_full_outputs": {"value": round(e2e_bytes_all / e2e_full_time_max / 1e9, 3)
+                             if e2e_full_time_max and full_all else None, "unit": "GB/s",
+                             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h_full),
+                             "note": "the e2e pass with every output array copied back"},
+        "cross_rank_timing": cross_rank, "host_wall_s": round(wall, 3),
+        "workload_description": " | ".join(wl.description for wl, _, _ in parts),
+    }
+    detail_path = Path(args.detail)
+    try:
+        detail_path.parent.mkdir(parents=True, exist_ok=True)
+        detail_path.write_text(json.dumps(detail, indent=1, default=str) + "\n")
+        detail_ref = str(detail_path.relative_to(ROOT) if detail_path.is_relative_to(ROOT)
+                         else detail_path)
+    except OSError as e:
+        detail_ref = f"unwritten: {e}"
+    me = model_eval if isinstance(model_eval, dict) else {}
     line = {
-        "metric": "suite GB/s", "value": round(value, 3), "unit": "GB/s", "n_gpus": dist.world,
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": dist.world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(elapsed_max / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (deterministic seed pattern, tests/support.hpp:35-44)",
-        "config": {"workload": args.workload,
-                   "description": " | ".join(wl.description for wl, _, _ in parts),
-                   "kernels": len(kernels),
-                   "calibration_kernels": n_cal, "application_kernels": n_app,
-                   "trials_per_kernel": args.steps * args.trials_per_step,
-                   "l2": "no flush: every kernel's trials run back to back as the reference's "
-                         "measure_kernel times them (executor.cpp:40-48; warm caches for the small "
-                         "application sizes are part of what the model predicts); the HBM "
-                         "microbenchmarks use arrays >= 1 GiB and the largest application sizes "
-                         "exceed the 126 MB L2 (matmul 8192: 256 MB per array, DG 10^6: 0.25-2 GB)",
-                   "parallelism": f"(kernel, trial) units LPT-sharded over {dist.world} rank(s)"},
-        "suite_hbm_GBps": round(hbm_b / hbm_t / 1e9, 1) if hbm_t else None,
-        "suite_flops_TFps": round(fl / fl_t / 1e12, 2) if fl_t else None,
-        "models": models,
-        # headline: per application variant, from each workload's headline
-        # model and its GPU fit with the lowest CALIBRATION error
-        "geomean_rel_error": {v: e for h in heads.values()
-                              for v, e in (h["geomean_rel_error"] or {}).items()},
-        "geomean_rel_error_by_application": {w: h["geomean_rel_error_all"]
-                                             for w, h in heads.items()},
-        "ranking_correct": {w: h["ranking_correct"] for w, h in heads.items()},
-        "ranking_correct_gap_ge_2pct": {w: h["ranking_correct_gap_ge_2pct"]
-                                        for w, h in heads.items()},
-        "headline": heads,
-        "roofline": roofline,
-        "model_eval": model_eval,
-        "tensor_variant": tensor_variant,
-        "overlap_diagnosis": diagnosis,
-        "roofline_hbm": roofline_hbm,
-        "suite_rooflines": suite_rooflines,
-        "cpu_baseline": cpu_gmem_sample() if dist.world == 1 else None,
-        # the reference library itself on the host cores (modelling path)
-        "cpu_baseline_reference": reference_model_sample() if dist.world == 1 else None,
+        "config": bench_config(args.workload, len(kernels), n_cal, n_app,
+                               args.steps * args.trials_per_step, dist.world),
+        "roofline": {k: roofline.get(k) for k in ("bound", "achieved", "peak", "unit", "frac",
+                                                   "traffic", "kernel", "share_of_step")},
+        "roofline_binding": ({k: roofline["binding_roofline"][k]
+                              for k in ("bound", "achieved", "peak", "unit", "frac")}
+                             if roofline.get("binding_roofline") else None),
+        "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_bytes_all / e2e_time_max / 1e9, 3) if e2e_time_max else None,
-                "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "kernels": int(e2e_kernels),
-                "note": "ps_run_host_batch_ex: every kernel's inputs H2D from pinned host memory each "
-                        "step, the kernels, and the step's result (one device checksum of each "
-                        "kernel's outputs) D2H; copy-in, launch and read-back pipelined on three "
-                        "streams over four device slots"},
-        "e2e_full_outputs": {"value": round(e2e_bytes_all / e2e_full_time_max / 1e9, 3)
-                             if e2e_full_time_max and full_all else None, "unit": "GB/s",
-                             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h_full),
-                             "note": "the same with every output array copied back"
-                             + ("" if full_all else " (skipped: output arrays do not fit this "
-                                "host's pinned memory share)")},
-        # sweep launches (all ranks) + per e2e step: every rank's checksum
-        # pass (kernels + checksum launches) and full-output pass
-        "gpu_launches": int(len(table) + args.steps * e2e_launches),
-        "cross_rank_timing": cross_rank,
-        "clocks": clocks,
-        "host_wall_s": round(wall, 3),
+                "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "accuracy": {
+            "geomean_rel_error": {v: e for h in heads.values()
+                                  for v, e in (h["geomean_rel_error"] or {}).items()},
+            "by_application": {w: h["geomean_rel_error_all"] for w, h in heads.items()},
+            "ranking_correct": {w: h["ranking_correct"] for w, h in heads.items()},
+            "ranking_correct_gap_ge_2pct": {w: h["ranking_correct_gap_ge_2pct"]
+                                            for w, h in heads.items()},
+            "model": {w: f"{h['model']}/{h['fit']}" for w, h in heads.items()}},
+        "model_eval": {k: me.get(k) for k in ("evaluations", "gpu_evals_per_s",
+                                              "gpu_e2e_evals_per_s", "argmin_mismatches_vs_cpu",
+                                              "reference_predict_evals_per_s")} if me else None,
+        "gpu_launches": e2e_launch_total,
+        "clocks": {k: clocks.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+        "detail": detail_ref,
     }
-    print(json.dumps(line), flush=True)
+    out = json.dumps(line)
+    if len(out) > 4096:  # keep the line parseable: drop the largest optional parts
+        for k in ("model_eval", "roofline_binding"):
+            line.pop(k, None)
+            out = json.dumps(line)
+            if len(out) <= 4096:
+                break
+    print(out, flush=True)
     dev.close()
 
 
@@ -1087,6 +1133,8 @@ def main() -> None:
     ap.add_argument("--tc", type=int, default=1, help="report the tcgen05 variant (0: skip)")
     ap.add_argument("--c5-points", type=int, default=1_000_000,
                     help="parameter points for the model-evaluation report (0: skip)")
+    ap.add_argument("--detail", default=str(ROOT / "gpurun_out" / "bench_detail.json"),
+                    help="side file for the full report (models, diagnosis, per-family rooflines)")
     ap.add_argument("--headline-model", default="",
                     help="model whose GPU fit is the headline (default: the workload's)")
     args = ap.parse_args()
