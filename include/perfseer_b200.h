@@ -245,6 +245,11 @@ int ps_fit_lm_batched_ex(ps_ctx* ctx, const ps_bytecode* model, const ps_bytecod
                          const ps_fit_opts* opts, int mode, double* params_inout,
                          ps_fit_stats* stats);
 
+/* The device tanh K17 and K18 evaluate sstep/tanh with (csrc/cuda/libm_glibc.cuh):
+ * the host glibc's std::tanh (model.cpp:253) restated bit for bit, so device
+ * and reference model evaluations agree exactly. x, out: n host doubles. */
+int ps_math_tanh(ps_ctx* ctx, const double* x, int64_t n, double* out);
+
 /* K18 batched prediction over a variant space. A table set is compiled
  * host-side from JSON {"variants": [{"id": variant id, "model": model text,
  * "params": [fitted values], "group": application index, "coords":
@@ -276,6 +281,10 @@ int ps_catalog(const char* catalog, const char* tags, const char* match, char* o
                size_t* needed);
 /* parse_model_file (model.cpp:625-644) -> JSON {output, expression, params,
  * features, cost_params}. */
+/* One catalog kernel as {"id", "kernel": perfseer-kernel/1 JSON
+ * (kernel_json.cpp:135-196), "bindings"} — what the reference's
+ * kernel_from_json + analyze consume (stage-file interop). */
+int ps_kernel_json(const char* variant_id, char* out, size_t cap, size_t* needed);
 int ps_model_info(const char* model_text, char* out, size_t cap, size_t* needed);
 /* gather_feature_values (features.cpp:473-493) for the model's features over
  * kernels given by variant id: out[k * nf + f]. */

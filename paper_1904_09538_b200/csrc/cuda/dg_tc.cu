@@ -183,7 +183,8 @@ struct Cfg {
   // 4 at 48-96 (6-8 cost 5-13% there), 6 at Np >= 112
   // (one matrix per CTA: 5.4 -> 6.1 TB/s at Np = 128 against 4 stages).
   // Build-time knobs for such sweeps: DGTC_STAGES, DGTC_EPI / DGTC_EPI8_MASK
-  // (8 epilogue warps: +4% at Np = 16, none at 32, losses at 48/96), DGTC_ORDER (1 = blocked tile order: 2-8% slower everywhere),
+  // (8 epilogue warps: +4% at Np = 16, +1-5% at 32 with the 3-stage ring, losses at 48/96;
+  // on at Np = 16 and 32, DGTC_EPI8_MASK = 3), DGTC_ORDER (1 = blocked tile order: 2-8% slower everywhere),
   // DGTC_CPS (2 = two CTAs per SM at Np <= 32: within noise), DGTC_SUB_MASK
   // (256-row tiles as two M = 128 sub-tiles; on at Np = 64 only).
   // CTAs per SM: two at Np <= 32 when DGTC_CPS == 2 (smaller ring and buffers)

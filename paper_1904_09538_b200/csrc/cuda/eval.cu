@@ -14,13 +14,11 @@
 #include <cstring>
 #include <vector>
 
+#include "libm_glibc.cuh"
 #include "runtime_internal.h"
 
 namespace ps {
 
-constexpr int kEvalMaxFeat = 48;
-constexpr int kEvalMaxGroups = 8;
-constexpr int kEvalMaxStack = 48;
 
 struct DevTables {
   FlatTables t;  // pointers are device pointers
@@ -37,7 +35,7 @@ __device__ double eval_model_bc(const int32_t* ops, int n_ops, const double* con
       case PS_BC_NUM: st[sp++] = consts[arg]; break;
       case PS_BC_PARAM: st[sp++] = p[arg]; break;
       case PS_BC_FEAT: st[sp++] = f[arg]; break;
-      case PS_BC_TANH: st[sp - 1] = tanh(st[sp - 1]); break;
+      case PS_BC_TANH: st[sp - 1] = glibc_tanh(st[sp - 1]); break;
       default: {
         const double b = st[--sp], a = st[sp - 1];
         st[sp - 1] = code == PS_BC_ADD ? __dadd_rn(a, b)
@@ -109,8 +107,17 @@ __global__ void __launch_bounds__(128) eval_points_kernel(FlatTables t, const in
 int eval_tables_gpu(Ctx* c, const FlatTables& h, const int64_t* points, int64_t npts, double* pred,
                     uint8_t* argmin, double* kernel_seconds) {
   if (h.ngroups > kEvalMaxGroups) return set_error(PS_ERR_ARG, "at most %d application groups", kEvalMaxGroups);
-  for (int m = 0; m < h.nmodels; ++m)
+  if (h.nvar > kEvalMaxVariants) return set_error(PS_ERR_ARG, "at most %d variants", kEvalMaxVariants);
+  for (int m = 0; m < h.nmodels; ++m) {
     if (h.model_nf[m] > kEvalMaxFeat) return set_error(PS_ERR_ARG, "model with more than %d features", kEvalMaxFeat);
+    const int np = h.model_param_begin[m + 1] - h.model_param_begin[m];
+    const int depth = bytecode_depth(h.ops + h.model_op_begin[m], h.model_op_begin[m + 1] - h.model_op_begin[m],
+                                     h.model_const_begin[m + 1] - h.model_const_begin[m], np, h.model_nf[m]);
+    if (depth < 0) return set_error(PS_ERR_ARG, "model %d: malformed bytecode", m);
+    if (depth > kEvalMaxStack)
+      return set_error(PS_ERR_ARG, "model %d: expression needs a stack of %d (device evaluator: %d)", m, depth,
+                       kEvalMaxStack);
+  }
   if (cudaSetDevice(c->device) != cudaSuccess) return set_error(PS_ERR_CUDA, "cudaSetDevice failed");
   // Pack every table array into one device allocation.
   struct Part {

@@ -14,15 +14,15 @@
 // (s = |initial p|) runs the same iteration in scaled coordinates.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
+#include "libm_glibc.cuh"
 #include "runtime_internal.h"
 
 namespace ps {
 
-constexpr int kLmMaxParams = 24;
-constexpr int kLmMaxStack = 48;
 constexpr int kLmThreads = 256;
 
 struct LmProgram {
@@ -41,7 +41,7 @@ __device__ double run_program(const LmProgram& pr, const double* p, const double
       case PS_BC_NUM: st[sp++] = pr.consts[arg]; break;
       case PS_BC_PARAM: st[sp++] = p[arg]; break;
       case PS_BC_FEAT: st[sp++] = f[arg]; break;
-      case PS_BC_TANH: st[sp - 1] = tanh(st[sp - 1]); break;
+      case PS_BC_TANH: st[sp - 1] = glibc_tanh(st[sp - 1]); break;
       default: {
         const double b = st[--sp], a = st[sp - 1];
         st[sp - 1] = code == PS_BC_ADD ? __dadd_rn(a, b)
@@ -59,7 +59,6 @@ __device__ double run_program(const LmProgram& pr, const double* p, const double
 // one pass yields g and dg/dp without the symbolic derivative trees (which
 // grow combinatorially for nested overlap steps). The product, quotient and
 // tanh rules are the ones diff_expr applies (model.cpp:289-330).
-constexpr int kDualStack = 24;
 __device__ void run_dual(const LmProgram& pr, const double* p, const double* f, int np, double* val,
                          double* grad) {
   double sv[kDualStack];
@@ -81,7 +80,7 @@ __device__ void run_dual(const LmProgram& pr, const double* p, const double* f, 
         ++sp;
         break;
       case PS_BC_TANH: {
-        const double t = tanh(sv[sp - 1]);
+        const double t = glibc_tanh(sv[sp - 1]);
         const double d = 1.0 - t * t;
         sv[sp - 1] = t;
         for (int j = 0; j < np; ++j) sg[sp - 1][j] = d * sg[sp - 1][j];
@@ -354,7 +353,64 @@ __global__ void __launch_bounds__(kLmThreads) lm_batched_kernel(LmArgs A) {
 
 }  // namespace ps
 
+namespace ps {
+
+int bytecode_depth(const int32_t* ops, int n_ops, int n_consts, int np, int nf) {
+  if (n_ops < 1 || !ops) return -1;
+  int sp = 0, depth = 0;
+  for (int i = 0; i < n_ops; ++i) {
+    const int code = ops[i] >> 16, arg = ops[i] & 0xffff;
+    switch (code) {
+      case PS_BC_NUM:
+      case PS_BC_PARAM:
+      case PS_BC_FEAT:
+        if (arg >= (code == PS_BC_NUM ? n_consts : code == PS_BC_PARAM ? np : nf)) return -1;
+        depth = std::max(depth, ++sp);
+        break;
+      case PS_BC_TANH:
+        if (sp < 1) return -1;
+        break;
+      case PS_BC_ADD:
+      case PS_BC_SUB:
+      case PS_BC_MUL:
+      case PS_BC_DIV:
+        if (sp < 2) return -1;
+        --sp;
+        break;
+      default:
+        return -1;
+    }
+  }
+  return sp == 1 ? depth : -1;
+}
+
+__global__ void tanh_kernel(const double* x, int64_t n, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = glibc_tanh(x[i]);
+}
+
+}  // namespace ps
+
 using namespace ps;
+
+extern "C" int ps_math_tanh(ps_ctx* ctx, const double* x, int64_t n, double* out) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !x || !out || n < 0) return set_error(PS_ERR_ARG, "ps_math_tanh: bad argument");
+  if (n == 0) return PS_OK;
+  cudaSetDevice(c->device);
+  const size_t bytes = sizeof(double) * (size_t)n;
+  int rc = c->ensure(c->scratch[0], 2 * bytes + 256);
+  if (rc) return rc;
+  double* dx = static_cast<double*>(c->scratch[0].ptr);
+  double* dy = dx + n;
+  cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, c->stream);
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
+  tanh_kernel<<<blocks, 256, 0, c->stream>>>(dx, n, dy);
+  cudaMemcpyAsync(out, dy, bytes, cudaMemcpyDeviceToHost, c->stream);
+  const cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "tanh kernel failed: %s", cudaGetErrorString(e));
+  return PS_OK;
+}
 
 extern "C" int ps_fit_lm_batched_ex(ps_ctx* ctx, const ps_bytecode* model, const ps_bytecode* jac,
                                     int np, int nf, const double* features, const double* t, int nr,
@@ -371,6 +427,24 @@ extern "C" int ps_fit_lm_batched_ex(ps_ctx* ctx, const ps_bytecode* model, const
                      "cannot have full column rank",
                      nr, np);
   if (nbatch < 1) return set_error(PS_ERR_ARG, "nbatch must be >= 1");
+  if (nf < 1 || nf > 0xffff) return set_error(PS_ERR_ARG, "nf must be in 1..65535");
+  {
+    // the device interpreters keep fixed stacks: reject deeper programs here
+    const int dm = bytecode_depth(model->ops, model->n_ops, model->n_consts, np, nf);
+    if (dm < 0) return set_error(PS_ERR_ARG, "malformed model bytecode");
+    const int lim = dual ? kDualStack : kLmMaxStack;
+    if (dm > lim)
+      return set_error(PS_ERR_ARG, "model expression needs a stack of %d (device %s evaluator: %d)", dm,
+                       dual ? "forward-mode" : "bytecode", lim);
+    if (!dual)
+      for (int i = 0; i < np; ++i) {
+        const int dj = bytecode_depth(jac[i].ops, jac[i].n_ops, jac[i].n_consts, np, nf);
+        if (dj < 0) return set_error(PS_ERR_ARG, "malformed derivative bytecode for parameter %d", i);
+        if (dj > kLmMaxStack)
+          return set_error(PS_ERR_ARG, "derivative %d needs a stack of %d (device evaluator: %d)", i, dj,
+                           kLmMaxStack);
+      }
+  }
   cudaSetDevice(c->device);
   // Device copies: programs, features, t, params, stats.
   std::vector<const ps_bytecode*> progs{model};

@@ -103,6 +103,21 @@ struct FlatTables {
   const double* params;
 };
 
+// Device evaluator limits (K18 eval.cu, K17 lm.cu); the C ABI rejects inputs
+// beyond them before any launch.
+constexpr int kEvalMaxFeat = 48;
+constexpr int kEvalMaxGroups = 8;
+constexpr int kEvalMaxStack = 48;
+constexpr int kEvalMaxVariants = 256;  // argmin is one byte per group
+constexpr int kLmMaxParams = 24;
+constexpr int kLmMaxStack = 48;
+constexpr int kDualStack = 24;
+
+// Deepest stack a postfix program reaches; -1 when it underflows, ends with
+// other than one value, or references a constant/parameter/feature outside
+// [0, n_consts) / [0, np) / [0, nf).
+int bytecode_depth(const int32_t* ops, int n_ops, int n_consts, int np, int nf);
+
 int eval_tables_gpu(Ctx* c, const FlatTables& t, const int64_t* points, int64_t npts, double* pred,
                     uint8_t* argmin, double* kernel_seconds);
 

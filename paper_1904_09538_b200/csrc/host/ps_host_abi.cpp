@@ -11,6 +11,7 @@
 #include "ps_catalog.hpp"
 #include "ps_enumerate.hpp"
 #include "ps_executor.hpp"
+#include "ps_json.hpp"
 #include "ps_model.hpp"
 
 using namespace perfseer;
@@ -85,6 +86,18 @@ int ps_catalog(const char* catalog, const char* tags, const char* match, char* o
     std::string s;
     for (const auto& g : kernels) s += g.id + "\t" + bindings_str(g.bindings) + "\n";
     return copy_out(s, out, cap, needed);
+  });
+}
+
+int ps_kernel_json(const char* variant_id, char* out, size_t cap, size_t* needed) {
+  return guarded([&] {
+    if (!variant_id) throw EvalError("ps_kernel_json: null variant id");
+    GeneratedKernel g = kernel_from_variant_id(variant_id);
+    nlohmann::json j;
+    j["id"] = g.id;
+    j["kernel"] = kernel_to_json(g.kernel);
+    j["bindings"] = g.bindings;
+    return copy_out(j.dump(), out, cap, needed);
   });
 }
 

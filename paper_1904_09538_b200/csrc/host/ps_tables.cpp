@@ -50,27 +50,35 @@ VariantTables build_variant_tables(const std::string& spec_json) {
     Model m = parse_model_file(text);
     auto counts = analyze_cached(g.kernel);
 
+    // One compiled model per (text, parameter values): the same model text
+    // calibrated on different machines (or runs) stays distinct.
+    std::vector<double> p = v.at("params").get<std::vector<double>>();
+    if (p.size() != m.params.size())
+      throw EvalError("variant '" + id + "': " + std::to_string(p.size()) + " params for a model with " +
+                      std::to_string(m.params.size()));
+    std::string key = text;
+    key.push_back('\0');
+    for (double x : p) key.append(reinterpret_cast<const char*>(&x), sizeof x);
     int mi;
-    auto it = model_index.find(text);
+    auto it = model_index.find(key);
     if (it == model_index.end()) {
       mi = int(t.models.size());
-      model_index[text] = mi;
+      model_index[key] = mi;
       t.models.push_back(compile_bytecode(m.expr));
-      std::vector<double> p = v.at("params").get<std::vector<double>>();
-      if (p.size() != m.params.size())
-        throw EvalError("variant '" + id + "': " + std::to_string(p.size()) + " params for a model with " +
-                        std::to_string(m.params.size()));
       t.params.push_back(p);
       t.model_nf.push_back(int(m.features.size()));
     } else {
       mi = it->second;
     }
+    const int group = v.value("group", 0);
+    if (group < 0 || group >= 8)
+      throw EvalError("variant '" + id + "': group " + std::to_string(group) + " outside 0..7");
     std::map<std::string, int> coords;
     for (const auto& [name, c] : v.at("coords").items()) coords[name] = c.get<int>();
     for (const auto& p : g.kernel.domain.parameters)
       if (!coords.count(p)) throw EvalError("variant '" + id + "': parameter '" + p + "' has no point coordinate");
 
-    t.var_group.push_back(v.value("group", 0));
+    t.var_group.push_back(group);
     t.var_model.push_back(mi);
     t.var_id.push_back(id);
     t.var_feat_base.push_back(int(t.feat_begin.size()));
@@ -104,6 +112,11 @@ VariantTables build_variant_tables(const std::string& spec_json) {
     }
   }
   for (int g : t.var_group) t.ngroups = std::max(t.ngroups, g + 1);
+  if (t.var_model.size() > 256)
+    throw EvalError("at most 256 variants per table set (the argmin is one byte per group)");
+  for (const auto& bc : t.models)
+    if (bc.max_stack > 48) throw EvalError("model expression needs a stack of " + std::to_string(bc.max_stack) +
+                                           " (device evaluator: 48)");
   return t;
 }
 

@@ -19,6 +19,8 @@ def _declare() -> C.CDLL:
     L.ps_catalog.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_size_t,
                              _P(C.c_size_t)]
     L.ps_model_info.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, _P(C.c_size_t)]
+    L.ps_kernel_json.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, _P(C.c_size_t)]
+    L.ps_kernel_json.restype = C.c_int
     L.ps_feature_table.argtypes = [C.c_char_p, C.c_char_p, C.c_int, _P(C.c_double), C.c_int64]
     L.ps_fit_cpu.argtypes = [C.c_char_p, _P(C.c_double), _P(C.c_double), C.c_int, C.c_int,
                              _P(FitOpts), _P(C.c_double), _P(FitStats)]
@@ -67,6 +69,13 @@ def catalog(tags: list[str], match: str = "superset", which: str = "b200") -> li
             bind[k] = int(v)
         out.append((vid, bind))
     return out
+
+
+def kernel_json(variant_id: str) -> dict:
+    """{"id", "kernel" (perfseer-kernel/1), "bindings"} of a catalog variant."""
+    import json
+    L = _declare()
+    return json.loads(_string_call(L.ps_kernel_json, variant_id.encode()))
 
 
 class HostModel:

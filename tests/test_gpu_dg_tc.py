@@ -76,3 +76,16 @@ def test_dg_tc_cta_pairs(dev, monkeypatch, nel, np_, nmat):
     ins = make_inputs(d, io, "seed17")
     np.testing.assert_array_equal(dev.run(d, ins)[0].view(np.uint32),
                                   oracle_suite.run(d, io, ins)[0].view(np.uint32))
+
+
+@pytest.mark.parametrize("np_", [16, 32])
+def test_dg_tc_ring_wraps_bitwise(dev, np_):
+    """enough tiles per persistent CTA (>= 10 x 148 x 128 rows)
+    that the u ring (8 stages at Np = 16, 3 at Np = 32) and the 8-warp
+    epilogue buffers wrap many times, so every empty-barrier phase is used."""
+    nel = 148 * 128 * 10 + 48  # plus a partial last tile
+    d, io = desc_io(_id(nel, np_))
+    ins = make_inputs(d, io, "seed17")
+    got = dev.run(d, ins)[0]
+    want = oracle_suite.run(d, io, ins)[0]
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))

@@ -71,3 +71,97 @@ def test_gpu_lm_rank_deficiency_is_an_error(dev):
     m = host.HostModel("f_exec_wall_time_d\np_a * f_thread_groups + p_b\n")
     with pytest.raises(PsError, match="rank deficiency"):
         fit_lm_batched(dev, m, np.ones((1, 1)), np.ones(1), np.ones((1, 2)))
+
+
+def test_device_tanh_is_glibc_tanh(dev):
+    """ps_math_tanh (the tanh inside K17/K18) returns the host libm's bits."""
+    import ctypes as C
+    import math
+
+    from paper_1904_09538_b200._abi import check, lib
+    rng = np.random.default_rng(11)
+    mag = np.exp(rng.uniform(-25.0, np.log(60.0), 200_000))
+    x = np.concatenate([mag * np.where(rng.random(mag.size) < 0.5, -1.0, 1.0),
+                        [0.0, -0.0, 1e-300, 5e-324, 0.5 * math.log(2), 1.5 * math.log(2), 1.0, -1.0,
+                         21.99, 22.0, 22.01, 40.0, -40.0, math.inf, -math.inf]])
+    want = np.array([math.tanh(v) for v in x])
+    got = np.empty_like(x)
+    L = lib()
+    L.ps_math_tanh.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double)]
+    L.ps_math_tanh.restype = C.c_int
+    check(L.ps_math_tanh(dev._ctx, x.ctypes.data_as(C.POINTER(C.c_double)), x.size,
+                         got.ctypes.data_as(C.POINTER(C.c_double))))
+    bad = np.flatnonzero(got.view(np.uint64) != want.view(np.uint64))
+    assert bad.size == 0, f"{bad.size} mismatches, e.g. x={x[bad[:3]]}"
+
+
+def _table_fits():
+    """Every model of every workload on the committed round-1 sweep table."""
+    import csv
+    rows = {}
+    with open(Path(__file__).resolve().parents[1] / "profiles" / "r01_table_all.csv") as f:
+        for r in csv.DictReader(f):
+            rows[r["kernel"]] = float(r["mean_seconds"])
+    from paper_1904_09538_b200 import workloads
+    cases = []
+    for wl in workloads.WORKLOADS.values():
+        for name in wl.models:
+            cases.append((wl.name, name))
+    return rows, cases
+
+
+_ROWS, _CASES = _table_fits()
+
+
+@pytest.mark.parametrize("case", _CASES, ids=lambda c: f"{c[0]}-{c[1]}")
+def test_gpu_lm_reference_mode_on_real_table(dev, case):
+    """K17 in reference mode (output-scaled rows, the
+    reference's start, row-order sums, glibc tanh) against fit_model
+    (model.cpp:485-606, the port verified bit-exact against the reference) on
+    the round-1 B200 calibration table: identical parameters."""
+    import bench
+    from paper_1904_09538_b200 import host, workloads
+    from paper_1904_09538_b200.device import fit_lm_batched
+    wname, mname = case
+    parts, _ = bench.workload_kernels(wname)
+    wl, cal, _app = parts[0]
+    cal = [k for k in cal if k in _ROWS]
+    m = host.HostModel(wl.models[mname])
+    fc = m.feature_table(cal)
+    tc = np.array([_ROWS[k] for k in cal])
+    try:
+        p_ref, st = m.fit_cpu(fc, tc, scale=True)
+    except Exception as e:  # the reference itself fails (e.g. divergence): nothing to match
+        pytest.skip(f"fit_model raises: {e}")
+    fs, ts = fc / tc[:, None], np.ones_like(tc)
+    pg, sg = fit_lm_batched(dev, m, fs, ts, m.initial_point(fs, ts, scale=0)[None], mode=0)
+    rel = np.max(np.abs(pg[0] - p_ref) / np.maximum(np.abs(p_ref), 1e-300))
+    assert rel <= 1e-4, f"max relative parameter difference {rel:.3g}"
+    assert sg[0]["iterations"] == st["iterations"]
+    np.testing.assert_array_equal(pg[0], p_ref)
+
+
+def test_lm_rejects_programs_deeper_than_the_device_stack(dev):
+    import ctypes as C
+
+    from paper_1904_09538_b200 import PsError
+    from paper_1904_09538_b200._abi import Bytecode, FitOpts, FitStats, check, lib
+    L = lib()
+    depth = 60  # push p0 60 times, then 59 adds
+    ops = np.array([(1 << 16) | 0] * depth + [3 << 16] * (depth - 1), dtype=np.int32)
+    consts = np.zeros(1)
+    bc = Bytecode(len(ops), 0, ops.ctypes.data_as(C.POINTER(C.c_int32)),
+                  consts.ctypes.data_as(C.POINTER(C.c_double)))
+    jac = (Bytecode * 1)(bc)
+    f = np.ones((1, 4, 1))
+    t = np.ones((1, 4))
+    p = np.ones((1, 1))
+    st = (FitStats * 1)()
+    o = FitOpts(1e-3, 0.1, 10.0, 1e-10, 1e-10, 200, 0)
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    L.ps_fit_lm_batched_ex.restype = C.c_int
+    rc = L.ps_fit_lm_batched_ex(dev._ctx, C.byref(bc), jac, 1, 1, dp(f), dp(t), 4, 1, C.byref(o), 0,
+                                dp(p), st)
+    assert rc != 0 and b"stack" in L.ps_last_error()
+    with pytest.raises(PsError):
+        check(rc)

@@ -43,3 +43,41 @@ def test_tables_equal_reference_predict_bitwise():
         cols = [i for i, v in enumerate(variants) if v["group"] == g]
         want = [cols[int(np.argmin(pred[j, cols]))] for j in range(len(pts))]
         assert list(arg[:, g]) == want
+
+
+def test_same_model_text_with_different_params_stays_distinct():
+    """one model calibrated twice (e.g. on two machines) must keep
+    both parameter vectors, not reuse the first."""
+    from paper_1904_09538_b200.predict import PredictionTables, c5_points
+    v = _variants("linear")[0]
+    a = dict(v, params=[1e-12] * len(v["params"]))
+    b = dict(v, params=[5e-12] * len(v["params"]), group=1)
+    t = PredictionTables([a, b])
+    pred, _ = t.eval_cpu(c5_points(4, seed=1))
+    np.testing.assert_allclose(pred[:, 1] / pred[:, 0], 5.0, rtol=1e-12)
+
+
+def test_tables_reject_out_of_range_groups_and_too_many_variants():
+    import pytest
+
+    from paper_1904_09538_b200 import PsError
+    from paper_1904_09538_b200.predict import PredictionTables
+    v = _variants("linear")[0]
+    for g in (-1, 8):
+        with pytest.raises(PsError, match="group"):
+            PredictionTables([dict(v, group=g)])
+    with pytest.raises(PsError, match="256 variants"):
+        PredictionTables([v] * 257)
+
+
+def test_tables_reject_models_deeper_than_the_device_stack():
+    import pytest
+
+    from paper_1904_09538_b200 import PsError
+    from paper_1904_09538_b200.predict import PredictionTables
+    v = _variants("linear")[0]
+    # a right-nested sum of 50 terms needs a 50-deep postfix stack
+    terms = " + (".join(f"p_{i} * f_thread_groups" for i in range(50)) + ")" * 49
+    text = "f_exec_wall_time_x\n" + terms + "\n"
+    with pytest.raises(PsError, match="stack"):
+        PredictionTables([dict(v, model=text, params=[1e-12] * 50)])
