@@ -45,3 +45,13 @@ $(OUT)/port_acceptance: $(ROOT)/tests/acceptance.cpp $(LIB)
 
 acceptance: $(OUT)/port_acceptance
 .PHONY: acceptance
+
+# The catalog pin (oracle/ref_catalog.cpp) against the port: its output must
+# equal tests/golden/catalog_reference.jsonl (the same program against the
+# reference) line for line. Needs only the port.
+$(OUT)/port_ref_catalog: $(ROOT)/oracle/ref_catalog.cpp $(LIB)
+	@mkdir -p $(OUT)
+	$(CXX) -std=c++20 -O2 -w -I$(ROOT)/paper_1904_09538_b200/csrc/host -I$(ROOT)/oracle/shim -I$(JSON_DIR) $< -L$(dir $(LIB)) -lperfseer_b200 -Wl,-rpath,$(dir $(LIB)) -o $@
+
+catalog: $(OUT)/port_ref_catalog
+.PHONY: catalog
