@@ -26,6 +26,8 @@ def lib() -> C.CDLL:
         _lib.ref_flops_value.restype = C.c_float
         _lib.ref_flops_value.argtypes = [C.c_int, C.c_int64]
         _lib.ref_threads.restype = C.c_int
+        _lib.ref_matmul_rows.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_int64, C.c_int64,
+                                         C.c_void_p]
         _lib.ref_set_threads.argtypes = [C.c_int]
     return _lib
 
@@ -63,6 +65,16 @@ def run(desc, io, inputs: list[np.ndarray]) -> list[np.ndarray]:
     if rc:
         raise ValueError(f"oracle has no restatement for generator {desc.gen}")
     return outs
+
+
+def matmul_rows(desc, inputs: list[np.ndarray], i0: int, i1: int) -> np.ndarray:
+    """Rows [i0, i1) of the matmul oracle (same per-element fma order)."""
+    dt = np.float32 if desc.dtype == 0 else np.float64
+    ins = [np.ascontiguousarray(a, dtype=dt).reshape(-1) for a in inputs]
+    out = np.zeros((i1 - i0) * desc.n, dtype=dt)
+    ip = (C.c_void_p * 2)(*[a.ctypes.data for a in ins])
+    lib().ref_matmul_rows(C.addressof(desc), ip, i0, i1, out.ctypes.data)
+    return out
 
 
 def threads() -> int:

@@ -50,7 +50,7 @@ for tile, ns in (("16x16", (14, 28, 112, 1960, 2744)), ("18x18", (16, 48, 112, 2
         for keep in ("u", "res"):
             CASES.append(vid("finite_diff_rm", dtype="float32", tile=tile, keep=keep, n=n))
 for variant in ("noPF", "uPF", "dmPF", "dmPFtrans"):
-    for nel, np_ in ((32, 16), (48, 64), (16, 128), (32, 48), (16, 96)):
+    for nel, np_ in ((32, 16), (48, 64), (16, 128), (32, 48), (16, 96), (48, 32)):
         CASES.append(vid("dg_diff", dtype="float32", variant=variant, nelements=nel,
                          nunit_nodes=np_, nmatrices=3))
         for keep in ("u", "dm", "res"):
