@@ -313,6 +313,11 @@ int ps_model_bytecode(const char* model_text, int which, int32_t* ops, int cap_o
  * brute_force_count), 2 = the same enumeration on the GPU of ctx. */
 int ps_enumerate(ps_ctx* ctx, const char* variant_id, int mode, char* out, size_t cap,
                  size_t* needed);
+/* Process-wide options: "partial_subgroups" = strict (the reference: raise
+ * when a work-group is not a whole number of sub-groups) | round_up
+ * (ceil(wg/32) sub-groups); "launch_geometry" = realised
+ * (vectorised row sweeps, FD strips) | literal (one CTA per IR work-group,
+ * the grid/block of launch_geometry, transforms.cpp:242-275). */
 int ps_set_option(const char* key, const char* value);
 /* geo_mean_rel_error (executor.cpp:50-61). */
 int ps_geo_mean_rel_error(const double* pred, const double* meas, int n, double* out);

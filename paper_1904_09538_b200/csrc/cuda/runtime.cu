@@ -7,6 +7,8 @@
 // per-trial seconds, SPEC.md:547-549, 60 trials by default).
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -519,6 +521,15 @@ int prepare(Ctx* c, const ps_kernel_desc* d, int fill_mode, uint64_t seed) {
 // ---------------------------------------------------------------------------
 // Launch dispatch.
 
+// Launch geometry: "realised" (default: vectorised row sweeps for the
+// contiguous streams, FD strips of R work-groups per CTA) or "literal" (one
+// CTA per IR work-group, the grid/block launch_geometry defines,
+// transforms.cpp:242-275). ps_set_option("launch_geometry", ...) switches every
+// context; PS_GMEM_GENERIC=1 switches one at ps_init.
+static std::atomic<bool> g_literal_geometry{false};
+void set_literal_geometry(bool on) { g_literal_geometry.store(on); }
+bool literal_geometry() { return g_literal_geometry.load(); }
+
 static Pattern make_pattern(const ps_kernel_desc* d) {
   Pattern p;
   p.s0 = d->lid_stride0;
@@ -532,6 +543,7 @@ static Pattern make_pattern(const ps_kernel_desc* d) {
 
 int launch(Ctx* c, const ps_kernel_desc* d) {
   cudaStream_t st = c->stream;
+  const bool literal = c->force_generic || g_literal_geometry.load();
   void* in0 = c->in[0].ptr;
   void* in1 = c->in[1].ptr;
   void* out0 = c->out[0].ptr;
@@ -540,7 +552,7 @@ int launch(Ctx* c, const ps_kernel_desc* d) {
       Pattern p = make_pattern(d);
       const int64_t groups = p.G0 * p.G1;
       if (groups > INT32_MAX) return set_error(PS_ERR_ARG, "too many work-groups");
-      if (p.s0 == 1 && d->dtype == PS_F32 && d->nelements % 4 == 0 && !c->force_generic) {
+      if (p.s0 == 1 && d->dtype == PS_F32 && d->nelements % 4 == 0 && !literal) {
         // Contiguous index set [0, E): row-sweeping vectorised realisation.
         constexpr int ROWS = 4;
         const int64_t vecs = d->nelements / 4;
@@ -603,7 +615,7 @@ int launch(Ctx* c, const ps_kernel_desc* d) {
       break;
     case PS_GEN_OVERLAP: {
       Pattern p = make_pattern(d);
-      if (p.s0 == 1 && d->nelements % 4 == 0 && !c->force_generic) {
+      if (p.s0 == 1 && d->nelements % 4 == 0 && !literal) {
         constexpr int ROWS = 4;
         const int64_t vecs = d->nelements / 4;
         int64_t blocks = (vecs + 256 * ROWS - 1) / (256 * ROWS);
@@ -675,7 +687,7 @@ int launch(Ctx* c, const ps_kernel_desc* d) {
                     : ((int64_t)(groups + 15) / 16 * groups >= want) ? 16
                                                                       : 8;
       dim3 grid((groups + R - 1) / R, groups);
-      if (c->force_generic) {
+      if (literal) {
         dim3 g1(groups, groups);
         if (d->tile == 16)
           finite_diff<16><<<g1, block, 0, st>>>((const float*)in0, (float*)out0, n);
@@ -701,7 +713,20 @@ int launch(Ctx* c, const ps_kernel_desc* d) {
       const int R = (d->keep == PS_KEEP_U && (int64_t)(groups + 15) / 16 * groups >= want) ? 16 : 8;
       dim3 grid((groups + R - 1) / R, groups),
           block(d->tile == 16 ? fd_strip_threads<16>() : fd_strip_threads<18>());
-      if (d->keep == PS_KEEP_U) {
+      if (literal) {  // one T x T CTA per work-group
+        dim3 g1(groups, groups), b1(d->tile, d->tile);
+        if (d->keep == PS_KEEP_U) {
+          if (d->tile == 16)
+            finite_diff_rm_u<16><<<g1, b1, 0, st>>>((const float*)in0, (float*)out0, n);
+          else
+            finite_diff_rm_u<18><<<g1, b1, 0, st>>>((const float*)in0, (float*)out0, n);
+        } else {
+          if (d->tile == 16)
+            finite_diff_rm_res<16><<<g1, b1, 0, st>>>((float*)out0, n);
+          else
+            finite_diff_rm_res<18><<<g1, b1, 0, st>>>((float*)out0, n);
+        }
+      } else if (d->keep == PS_KEEP_U) {
         if (d->tile == 16) {
           if (R == 16)
             finite_diff_strip<16, 16, 1><<<grid, block, 0, st>>>((const float*)in0, (float*)out0, n);

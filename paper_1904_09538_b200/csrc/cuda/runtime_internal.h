@@ -118,6 +118,10 @@ constexpr int kDualStack = 24;
 // [0, n_consts) / [0, np) / [0, nf).
 int bytecode_depth(const int32_t* ops, int n_ops, int n_consts, int np, int nf);
 
+// Launch geometry switch (runtime.cu): literal = one CTA per IR work-group.
+void set_literal_geometry(bool on);
+bool literal_geometry();
+
 int eval_tables_gpu(Ctx* c, const FlatTables& t, const int64_t* points, int64_t npts, double* pred,
                     uint8_t* argmin, double* kernel_seconds);
 

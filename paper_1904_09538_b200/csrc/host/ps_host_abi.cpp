@@ -217,6 +217,11 @@ int ps_set_option(const char* key, const char* value) {
       clear_count_cache();
       return PS_OK;
     }
+    if (k == "launch_geometry") {
+      if (v != "realised" && v != "literal") throw EvalError("launch_geometry: realised | literal");
+      ps::set_literal_geometry(v == "literal");
+      return PS_OK;
+    }
     throw EvalError("unknown option '" + k + "'");
   });
 }

@@ -100,3 +100,23 @@ def test_errors_are_reported_not_silent(dev):
                         groups_fit="True", n=100), trials=1)
     with pytest.raises(PsError):
         dev.measure(vid("empty_knl", num_groups=4), trials=0)
+
+
+LITERAL = [c for c in CASES if c.split("__")[0] in ("gmem_pattern", "overlap_knl", "finite_diff",
+                                                    "finite_diff_rm")]
+
+
+@pytest.mark.parametrize("variant_id", LITERAL)
+def test_literal_launch_geometry_matches_oracle(dev, variant_id):
+    """launch_geometry=literal: one CTA per IR work-group (transforms.cpp:242-275)
+    instead of the vectorised/strip realisation; same values bit for bit."""
+    from paper_1904_09538_b200 import host
+    d, io = desc_io(variant_id)
+    ins = make_inputs(d, io, "uniform", seed=7)
+    host.set_option("launch_geometry", "literal")
+    try:
+        got = dev.run(d, ins)
+    finally:
+        host.set_option("launch_geometry", "realised")
+    for g, w in zip(got, oracle_suite.run(d, io, ins)):
+        np.testing.assert_array_equal(g.view(np.uint8), w.view(np.uint8), err_msg=variant_id)
