@@ -261,42 +261,69 @@ def summarize(times: list[float], factor: float = 5.0) -> tuple[float, int]:
     return sum(kept) / len(kept), len(kept)
 
 
-def _errors(wl, app, pred, ta) -> dict:
-    from paper_1904_09538_b200 import host, workloads
-    per_variant: dict[str, list] = {}
-    for vid, p, t in zip(app, pred, ta):
-        per_variant.setdefault(workloads.variant_of(vid, wl.variant_keys), []).append((p, t))
-    gm = {v: round(host.geo_mean_rel_error([p for p, _ in pts], [t for _, t in pts]), 5)
-          for v, pts in per_variant.items()}
-    # ranking per size: strict '<' first minimum (tools/perfseer.cpp:458-467)
+def _rank(wl, rows) -> dict:
+    """Per size: strict '<' first minimum (tools/perfseer.cpp:458-467) of the
+    prediction vs the measurement; rows = [(variant id, pred, meas)]."""
+    from paper_1904_09538_b200 import workloads
     by_size: dict[str, list] = {}
-    for vid, p, t in zip(app, pred, ta):
+    for vid, p, t in rows:
         by_size.setdefault(workloads.size_of(vid, wl.size_keys), []).append(
             (workloads.variant_of(vid, wl.variant_keys), p, t))
     ranks, clear, detail = [], [], {}
-    for size, rows in by_size.items():
-        if len(rows) < 2:
+    for size, rs in by_size.items():
+        if len(rs) < 2:
             continue
-        mbest = pbest = rows[0]
-        for r in rows:
+        mbest = pbest = rs[0]
+        for r in rs:
             if r[2] < mbest[2]:
                 mbest = r
             if r[1] < pbest[1]:
                 pbest = r
         ranks.append(mbest[0] == pbest[0])
         # measured gap between the fastest and the runner-up variant
-        ts = sorted(r[2] for r in rows)
+        ts = sorted(r[2] for r in rs)
         gap = (ts[1] - ts[0]) / ts[0]
         if gap >= 0.02:
             clear.append(mbest[0] == pbest[0])
         detail[size] = {"measured_best": mbest[0], "predicted_best": pbest[0],
                         "measured_gap": round(gap, 4)}
-    return {"geomean_rel_error": gm,
-            "geomean_rel_error_all": round(host.geo_mean_rel_error(pred, ta), 5),
-            "ranking_correct": f"{sum(ranks)}/{len(ranks)}",
+    return {"ranking_correct": f"{sum(ranks)}/{len(ranks)}",
             # sizes whose two fastest variants are >= 2% apart when measured
-            "ranking_correct_gap_ge_2pct": f"{sum(clear)}/{len(clear)}",
-            "ranking": detail}
+            "ranking_correct_gap_ge_2pct": f"{sum(clear)}/{len(clear)}", "ranking": detail}
+
+
+def _per_variant(wl, rows) -> dict:
+    from paper_1904_09538_b200 import host, workloads
+    per: dict[str, list] = {}
+    for vid, p, t in rows:
+        per.setdefault(workloads.variant_of(vid, wl.variant_keys), []).append((p, t))
+    return {v: round(host.geo_mean_rel_error([p for p, _ in pts], [t for _, t in pts]), 5)
+            for v, pts in per.items()}
+
+
+def _errors(wl, app, pred, ta) -> dict:
+    """Per-variant geomean |pred - meas| / meas and rankings over every
+    application size, plus the held-out split: `validation` = the workload's
+    validation sizes (used only to choose the headline model), `test` = the
+    rest (what the chosen model is scored on)."""
+    from paper_1904_09538_b200 import host, workloads
+    rows = list(zip(app, pred, ta))
+    out = {"geomean_rel_error": _per_variant(wl, rows),
+           "geomean_rel_error_all": round(host.geo_mean_rel_error(pred, ta), 5)}
+    out.update(_rank(wl, rows))
+    val = [r for r in rows if workloads.size_of(r[0], wl.size_keys) in wl.validation_sizes]
+    test = [r for r in rows if workloads.size_of(r[0], wl.size_keys) not in wl.validation_sizes]
+    if val and test:
+        out["validation_geomean_rel_error"] = round(host.geo_mean_rel_error(
+            [p for _, p, _ in val], [t for _, _, t in val]), 5)
+        rt = _rank(wl, test)
+        out["test"] = {"geomean_rel_error": _per_variant(wl, test),
+                       "geomean_rel_error_all": round(host.geo_mean_rel_error(
+                           [p for _, p, _ in test], [t for _, _, t in test]), 5),
+                       "ranking_correct": rt["ranking_correct"],
+                       "ranking_correct_gap_ge_2pct": rt["ranking_correct_gap_ge_2pct"],
+                       "rows": len(test)}
+    return out
 
 
 def _cal_err(m, params, cal, tc) -> float:
@@ -304,15 +331,25 @@ def _cal_err(m, params, cal, tc) -> float:
     return round(host.geo_mean_rel_error(m.predict_cpu(params, cal), tc), 5)
 
 
-def headline(models: dict, model: str) -> tuple[str | None, dict]:
-    """The GPU fit of the headline model with the smallest geomean relative
-    error on the CALIBRATION rows (application rows are never consulted)."""
-    fits = {k: v for k, v in models.get(model, {}).items()
-            if k.startswith("gpu_") and "calibration_geomean_rel_error" in v}
-    if not fits:
-        return None, {}
-    k = min(fits, key=lambda f: fits[f]["calibration_geomean_rel_error"])
-    return k, fits[k]
+def headline(models: dict, model: str = "") -> tuple[str | None, str | None, dict]:
+    """The headline (model, GPU fit). Held-out selection: among every
+    candidate model's GPU fits, the one with the lowest geomean error on the
+    workload's VALIDATION sizes; the test sizes are never consulted. Without
+    validation rows (or with `model` forced): that model's GPU fit with the
+    lowest CALIBRATION error."""
+    cands = []
+    for mname, fits in models.items():
+        if model and mname != model:
+            continue
+        for k, v in fits.items():
+            if k.startswith("gpu_") and "calibration_geomean_rel_error" in v:
+                key = (v["validation_geomean_rel_error"] if not model and
+                       "validation_geomean_rel_error" in v else v["calibration_geomean_rel_error"])
+                cands.append((key, mname, k, v))
+    if not cands:
+        return None, None, {}
+    _, mname, k, v = min(cands, key=lambda c: c[0])
+    return mname, k, v
 
 
 def model_report(wl, cal, app, mean_s: dict[str, float], dev=None) -> dict:
@@ -424,6 +461,48 @@ def overlap_diagnosis(parts, models: dict, mean_s: dict[str, float]) -> dict:
             per.setdefault(key, {})[workloads.size_of(vid, wl.size_keys)] = {
                 "full_s": full, "removed_s": removed, "onchip_s": est, "kind": kind}
         out[wl.name] = per
+    return out
+
+
+def _best_fit(fits: dict) -> dict:
+    """A model's GPU fit with the lowest calibration error."""
+    c = [v for k, v in fits.items() if k.startswith("gpu_") and "params" in v
+         and "calibration_geomean_rel_error" in v]
+    return min(c, key=lambda v: v["calibration_geomean_rel_error"]) if c else {}
+
+
+def paper_selection(parts, models: dict, diagnosis: dict, mean_s: dict[str, float]) -> dict:
+    """The paper's per-variant model choice:
+    the work-removal diagnosis (overlap_diagnosis, classify_overlap
+    executor.cpp:169-174) labels each application variant 'linear' or
+    'max_overlap' by majority over its sizes; a linear variant is predicted by
+    the linear model (Eq. 1), an overlapping one by the nonlinear model
+    (Eqs. 4-5), each with its best GPU fit."""
+    from paper_1904_09538_b200 import host, workloads
+    out = {}
+    for wl, _cal, app in parts:
+        diag = diagnosis.get(wl.name, {}) if isinstance(diagnosis, dict) else {}
+        fits = {m: _best_fit(models.get(wl.name, {}).get(m, {})) for m in ("linear", "nonlinear")}
+        if not all(fits.values()) or not diag:
+            continue
+        choice = {}
+        for var, by_size in diag.items():
+            kinds = [v["kind"] for v in by_size.values()]
+            choice[var] = "nonlinear" if kinds.count("max_overlap") * 2 > len(kinds) else "linear"
+        pred = {}
+        for mname in set(choice.values()):
+            m = host.HostModel(wl.models[mname])
+            p = np.array([fits[mname]["params"][n] for n in m.params])
+            pred[mname] = dict(zip(app, m.predict_cpu(p, app)))
+        rows = [(vid, pred[choice.get(workloads.variant_of(vid, wl.variant_keys), "linear")][vid]
+                 if choice.get(workloads.variant_of(vid, wl.variant_keys), "linear") in pred
+                 else pred[next(iter(pred))][vid], mean_s[vid]) for vid in app]
+        r = _rank(wl, rows)
+        out[wl.name] = {"choice": choice, "geomean_rel_error": _per_variant(wl, rows),
+                        "geomean_rel_error_all": round(host.geo_mean_rel_error(
+                            [p for _, p, _ in rows], [t for _, _, t in rows]), 5),
+                        "ranking_correct": r["ranking_correct"],
+                        "ranking_correct_gap_ge_2pct": r["ranking_correct_gap_ge_2pct"]}
     return out
 
 
@@ -1012,13 +1091,22 @@ def run_ours(args, dist: Dist) -> None:
     if dist.rank == 0:
         for wl, cal, app in parts:
             models[wl.name] = model_report(wl, cal, app, mean_s, dev)
-            hmodel = args.headline_model if args.headline_model in wl.models else wl.headline_model
-            hfit, head = headline(models[wl.name], hmodel)
+            forced = args.headline_model if args.headline_model in wl.models else ""
+            hmodel, hfit, head = headline(models[wl.name], forced)
+            if hmodel is None:  # no candidate fitted: fall back to the workload default
+                hmodel = wl.headline_model
             heads[wl.name] = {"model": hmodel, "fit": hfit,
+                              "selection": ("forced" if forced else
+                                            "held-out validation sizes" if
+                                            "validation_geomean_rel_error" in head
+                                            else "calibration error"),
+                              "validation_geomean_rel_error": head.get(
+                                  "validation_geomean_rel_error"),
                               "geomean_rel_error": head.get("geomean_rel_error"),
                               "geomean_rel_error_all": head.get("geomean_rel_error_all"),
                               "ranking_correct": head.get("ranking_correct"),
-                              "ranking_correct_gap_ge_2pct": head.get("ranking_correct_gap_ge_2pct")}
+                              "ranking_correct_gap_ge_2pct": head.get("ranking_correct_gap_ge_2pct"),
+                              "test": head.get("test")}
     try:
         variants = c5_variants(parts, models, heads) if dist.rank == 0 else None
         err = None
@@ -1037,6 +1125,10 @@ def run_ours(args, dist: Dist) -> None:
         diagnosis = overlap_diagnosis(parts, models, mean_s)
     except Exception as e:
         diagnosis = {"error": str(e)}
+    try:
+        paper = paper_selection(parts, models, diagnosis, mean_s)
+    except Exception as e:  # reported, not hidden
+        paper = {"error": str(e)}
     try:
         tensor_variant = tensor_variant_report(dev) if args.tc else None
         if args.tc and tensor_variant is not None and any(w.name == "dg" for w, _, _ in parts):
@@ -1057,7 +1149,8 @@ def run_ours(args, dist: Dist) -> None:
     ref_lib = reference_model_sample() if dist.world == 1 else None
     detail = {
         "models": models, "headline": heads, "model_eval": model_eval,
-        "overlap_diagnosis": diagnosis, "tensor_variant": tensor_variant,
+        "overlap_diagnosis": diagnosis, "paper_selection": paper,
+        "tensor_variant": tensor_variant,
         "roofline": roofline, "roofline_hbm": roofline_hbm, "suite_rooflines": suite_rooflines,
         "suite_hbm_GBps": round(hbm_b / hbm_t / 1e9, 1) if hbm_t else None,
         "suite_flops_TFps": round(fl / fl_t / 1e12, 2) if fl_t else None,
@@ -1095,13 +1188,24 @@ def run_ours(args, dist: Dist) -> None:
         "e2e": {"value": round(e2e_bytes_all / e2e_time_max / 1e9, 3) if e2e_time_max else None,
                 "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "accuracy": {
+            "model": {w: f"{h['model']}/{h['fit']}" for w, h in heads.items()},
+            "selection": {w: h["selection"] for w, h in heads.items()},
             "geomean_rel_error": {v: e for h in heads.values()
                                   for v, e in (h["geomean_rel_error"] or {}).items()},
             "by_application": {w: h["geomean_rel_error_all"] for w, h in heads.items()},
             "ranking_correct": {w: h["ranking_correct"] for w, h in heads.items()},
             "ranking_correct_gap_ge_2pct": {w: h["ranking_correct_gap_ge_2pct"]
                                             for w, h in heads.items()},
-            "model": {w: f"{h['model']}/{h['fit']}" for w, h in heads.items()}},
+            # the held-out sizes the headline model was NOT selected on
+            "test_geomean_rel_error": {v: e for h in heads.values()
+                                       for v, e in ((h.get("test") or {}).get(
+                                           "geomean_rel_error") or {}).items()},
+            "test_ranking_correct_gap_ge_2pct": {w: (h.get("test") or {}).get(
+                "ranking_correct_gap_ge_2pct") for w, h in heads.items()},
+            # the paper's own per-variant linear/nonlinear choice
+            "paper_model": ({w: {"all": v["geomean_rel_error_all"],
+                                 "ranking_gap_ge_2pct": v["ranking_correct_gap_ge_2pct"]}
+                             for w, v in paper.items()} if "error" not in paper else paper)},
         "model_eval": {k: me.get(k) for k in ("evaluations", "gpu_evals_per_s",
                                               "gpu_e2e_evals_per_s", "argmin_mismatches_vs_cpu",
                                               "reference_predict_evals_per_s")} if me else None,
@@ -1136,7 +1240,8 @@ def main() -> None:
     ap.add_argument("--detail", default=str(ROOT / "gpurun_out" / "bench_detail.json"),
                     help="side file for the full report (models, diagnosis, per-family rooflines)")
     ap.add_argument("--headline-model", default="",
-                    help="model whose GPU fit is the headline (default: the workload's)")
+                    help="force this model as the headline (default: held-out selection over "
+                         "every candidate model on the workload's validation sizes)")
     args = ap.parse_args()
     # the reference arm is CPU-only with no exchange (rank 0 alone runs it):
     # no process group, no GPU binding

@@ -14,6 +14,10 @@ OUTPUT = "f_exec_wall_time_cuda_b200_0"
 
 # Feature ids (reference grammar, features.cpp:124-249).
 G16 = "f_mem_access_global_float32_lstrides:{0:1;1:>1}_gstrides:{0:16;1:>16}_afr:1"
+# the same AFR-1 pattern split by direction (the gmem microbenchmarks with 1
+# and 2 input arrays separate a load from a store cost)
+G16L = "f_mem_access_global_float32_load_lstrides:{0:1;1:>1}_gstrides:{0:16;1:>16}_afr:1"
+G16S = "f_mem_access_global_float32_store_lstrides:{0:1;1:>1}_gstrides:{0:16;1:>16}_afr:1"
 OPS = {"add": "f_op_float32_add", "mul": "f_op_float32_mul", "madd": "f_op_float32_madd"}
 LMEM = "f_mem_access_local_float32"
 BAR = "f_sync_barrier_local"
@@ -111,6 +115,28 @@ def lsu2_model(hbm: list[tuple[str, str]], tags: list[tuple[str, str]],
             sharp_max(ch, sharp_max(cl, sharp_max(cops, cb, k), k), k) + "\n")
 
 
+def ldst_model(loads: list[tuple[str, str]], stores: list[tuple[str, str]],
+               ops: list[tuple[str, str]], lmem: list[tuple[str, str]], k: float = 40.0,
+               group_pipe: bool = False) -> str:
+    """launch (+ group) overhead + max(c_load + c_lmem, c_store, c_ops, c_barrier
+    [, c_group]): on sm_100 loads and shared-memory accesses occupy the
+    LSU/MIO pipe and L1, while global stores retire through the L2 write path
+    without holding the loads up (the DG variants' uncoalesced res stores
+    overlap their row loads: sum of the work-removed kernels >> full time);
+    the FP32 pipe and barriers overlap both. With group_pipe the per-group
+    launch cost is one more overlapping pipe instead of an additive term
+    (the CTA scheduler issues new groups while resident ones run)."""
+    cl = _sum([f"{p} * {f}" for p, f in loads] + [f"{p} * {f}" for p, f in lmem])
+    cs = _sum([f"{p} * {f}" for p, f in stores])
+    cops = _sum([f"{p} * {f}" for p, f in ops])
+    cb = f"p_bar * {BAR} * {GROUPS}"
+    cg = f"p_group * {GROUPS}"
+    inner = sharp_max(cops, sharp_max(cb, cg, k) if group_pipe else cb, k)
+    body = sharp_max(cl, sharp_max(cs, inner, k), k)
+    ovh = f"p_launch * {LAUNCH}" + ("" if group_pipe else f" + {cg}")
+    return OUTPUT + "\n" + ovh + " + " + body + "\n"
+
+
 def overlap3_model(gmem: list[tuple[str, str]], ops: list[tuple[str, str]],
                    lmem: list[tuple[str, str]]) -> str:
     """ovh + max(c_gmem, max(c_ops, c_lmem)): the paper's overlap form with the
@@ -149,12 +175,19 @@ class Workload:
     extra: dict = field(default_factory=dict)
     # C5 point column of each size parameter (predict.c5_points)
     c5_coords: dict = field(default_factory=lambda: {"n": 0})
-    # model whose GPU fit is the bench headline: the B200 LSU/FMA overlap model
+    # application sizes held out for model selection (workloads.size_of
+    # strings): the headline model is the candidate with the lowest geomean
+    # error on these, and its error is reported on the remaining sizes
+    validation_sizes: tuple[str, ...] = ()
+    # fallback headline when no validation sizes were measured
     headline_model: str = "lsu"
 
 
 MATMUL_GMEM = [("p_g16", G16), ("p_mmPFa", _tag("mm-PF-a")), ("p_mmPFb", _tag("mm-PF-b")),
                ("p_mmnoPFa", _tag("mm-noPF-a")), ("p_mmnoPFb", _tag("mm-noPF-b"))]
+
+MATMUL_LOADS = [("p_g16l", G16L)] + MATMUL_GMEM[1:]
+MATMUL_STORES = [("p_g16s", G16S)]
 
 MATMUL = Workload(
     name="matmul",
@@ -168,8 +201,12 @@ MATMUL = Workload(
             "overlap3": overlap3_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:]),
             "max3": max3_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:]),
             "lsu": lsu_model(MATMUL_GMEM, ONCHIP[:3], ONCHIP[3:]),
-            "lsu2": lsu2_model(MATMUL_GMEM[:1], MATMUL_GMEM[1:], ONCHIP[:3], ONCHIP[3:])},
+            "lsu2": lsu2_model(MATMUL_GMEM[:1], MATMUL_GMEM[1:], ONCHIP[:3], ONCHIP[3:]),
+            "ldst": ldst_model(MATMUL_LOADS, MATMUL_STORES, ONCHIP[:3], ONCHIP[3:]),
+            "ldst_g": ldst_model(MATMUL_LOADS, MATMUL_STORES, ONCHIP[:3], ONCHIP[3:],
+                                 group_pipe=True)},
     variant_keys=("prefetch",),
+    validation_sizes=("n=1024", "n=4096"),
     size_keys=("n",),
 )
 
@@ -177,6 +214,13 @@ G18 = "f_mem_access_global_float32_lstrides:{0:1;1:>1}_gstrides:{0:18;1:>18}_afr
 FD_GMEM = [("p_g16", G16), ("p_g18", G18),
            ("p_fd16u", _tag("fd-16x16-u")), ("p_fd16res", _tag("fd-16x16-res")),
            ("p_fd18u", _tag("fd-18x18-u")), ("p_fd18res", _tag("fd-18x18-res"))]
+
+# the 18x18 gmem benchmark has one input array only: its load and store counts
+# are collinear, so G18 stays undirected (with the loads)
+FD_LOADS = [("p_g16l", G16L), ("p_g18", G18), ("p_fd16u", _tag("fd-16x16-u")),
+            ("p_fd18u", _tag("fd-18x18-u"))]
+FD_STORES = [("p_g16s", G16S), ("p_fd16res", _tag("fd-16x16-res")),
+             ("p_fd18res", _tag("fd-18x18-res"))]
 
 FD = Workload(
     name="fd",
@@ -187,10 +231,14 @@ FD = Workload(
     calibration_tags=MICRO_TAGS + [["gmem_pattern_18"], ["finite_diff_rm"]],
     application_tags=[["finite_diff"]],
     models={"linear": linear_model(FD_GMEM, ONCHIP),
+            "nonlinear": overlap_model(FD_GMEM, ONCHIP),
             "max3": max3_model(FD_GMEM, ONCHIP[:3], ONCHIP[3:]),
             "lsu": lsu_model(FD_GMEM, ONCHIP[:3], ONCHIP[3:]),
-            "lsu2": lsu2_model(FD_GMEM[:2], FD_GMEM[2:], ONCHIP[:3], ONCHIP[3:])},
+            "lsu2": lsu2_model(FD_GMEM[:2], FD_GMEM[2:], ONCHIP[:3], ONCHIP[3:]),
+            "ldst": ldst_model(FD_LOADS, FD_STORES, ONCHIP[:3], ONCHIP[3:]),
+            "ldst_g": ldst_model(FD_LOADS, FD_STORES, ONCHIP[:3], ONCHIP[3:], group_pipe=True)},
     variant_keys=("tile",),
+    validation_sizes=("n=2240",),
     size_keys=("n",),
     extra={"options": {"partial_subgroups": "round_up"}},
     c5_coords={"n": 1},
@@ -199,6 +247,11 @@ FD = Workload(
 DG_TAGS = ["dg-noPF-u", "dg-noPF-res", "dg-uPFnoPF-dm", "dg-uPF-u", "dg-uPF-res", "dg-dmPF-dm",
            "dg-dmPF-u", "dg-dmPF-res", "dg-dmPFtrans-u", "dg-dmPFtrans-res"]
 DG_GMEM = [("p_g16", G16)] + [("p_" + t.replace("-", "_"), _tag(t)) for t in DG_TAGS]
+
+DG_LOADS = [("p_g16l", G16L)] + [("p_" + t.replace("-", "_"), _tag(t)) for t in DG_TAGS
+                                  if not t.endswith("-res")]
+DG_STORES = [("p_g16s", G16S)] + [("p_" + t.replace("-", "_"), _tag(t)) for t in DG_TAGS
+                                   if t.endswith("-res")]
 
 DG = Workload(
     name="dg",
@@ -210,10 +263,14 @@ DG = Workload(
     calibration_tags=MICRO_TAGS + [["dg_diff_rm"]],
     application_tags=[["dg_diff"]],
     models={"linear": linear_model(DG_GMEM, ONCHIP),
+            "nonlinear": overlap_model(DG_GMEM, ONCHIP),
             "max3": max3_model(DG_GMEM, ONCHIP[:3], ONCHIP[3:]),
             "lsu": lsu_model(DG_GMEM, ONCHIP[:3], ONCHIP[3:]),
-            "lsu2": lsu2_model(DG_GMEM[:1], DG_GMEM[1:], ONCHIP[:3], ONCHIP[3:])},
+            "lsu2": lsu2_model(DG_GMEM[:1], DG_GMEM[1:], ONCHIP[:3], ONCHIP[3:]),
+            "ldst": ldst_model(DG_LOADS, DG_STORES, ONCHIP[:3], ONCHIP[3:]),
+            "ldst_g": ldst_model(DG_LOADS, DG_STORES, ONCHIP[:3], ONCHIP[3:], group_pipe=True)},
     variant_keys=("variant",),
+    validation_sizes=tuple(f"nelements=100000;nunit_nodes={n}" for n in (16, 32, 48, 64, 96, 128)),
     size_keys=("nelements", "nunit_nodes"),
     c5_coords={"nelements": 2, "nunit_nodes": 3},
 )
@@ -221,12 +278,12 @@ DG = Workload(
 WORKLOADS = {w.name: w for w in (MATMUL, FD, DG)}
 # "all": one calibration sweep over the union of the three workloads' kernels
 # (BASELINE.json configs[3]); every workload's models are fitted on its own rows
-GROUPS = {"all": ["matmul", "fd", "dg"]}
+WORKLOAD_SETS = {"all": ["matmul", "fd", "dg"]}
 
 
 def resolve(name: str) -> list[Workload]:
-    if name in GROUPS:
-        return [WORKLOADS[n] for n in GROUPS[name]]
+    if name in WORKLOAD_SETS:
+        return [WORKLOADS[n] for n in WORKLOAD_SETS[name]]
     return [WORKLOADS[name]]
 
 
