@@ -352,74 +352,106 @@ def headline(models: dict, model: str = "") -> tuple[str | None, str | None, dic
     return mname, k, v
 
 
-def model_report(wl, cal, app, mean_s: dict[str, float], dev=None) -> dict:
-    """Fit every model of the workload on the measured calibration rows
-    (output-scaled, model.cpp:421-435) and predict the held-out application
-    rows. Two calibrations are reported: the reference-exact CPU fit
-    (fit_model from the reference's start) and the GPU batched LM (K17) run
-    as a multi-start batch (reference start + p_edge ladder, equilibrated),
-    keeping the start with the smallest residual."""
+EDGE_STARTS = (3.0, 10.0, 30.0, 100.0, 300.0, 1000.0)
+
+
+def model_reports(parts, mean_s: dict[str, float], dev=None) -> tuple[dict, dict]:
+    """Fit every model of every workload on its measured calibration rows and
+    predict the held-out application rows. Three calibrations per model:
+    * reference_fit: fit_model itself (the port, bit-exact with the
+      reference) on the output-scaled rows (model.cpp:421-435, 485-606);
+    * gpu_reference_fit: the same fit on the GPU (K17 reference mode: row-order
+      sums, the reference's start and trajectory; bit-identical);
+    * gpu_multistart_fit: the B200 calibration — relative residuals,
+      equilibrated columns, warp-shuffle sums, the relative-residual QR start
+      plus a p_edge ladder; the start with the smallest residual wins.
+    All GPU fits of the round (workloads x models x starts) run in ONE K17
+    launch (ps_fit_lm_jobs). Returns ({workload: {model: fits}}, K17 stats)."""
     from paper_1904_09538_b200 import host
-    out = {}
-    for mname, text in wl.models.items():
-        m = host.HostModel(text)
-        feats = m.feature_table(cal + app)
-        fc, fa = feats[: len(cal)], feats[len(cal):]
+    out: dict = {}
+    jobs, where = [], []
+    prep = {}
+    cpu_fit_s, cpu_fits = 0.0, 0
+    for wl, cal, app in parts:
+        out[wl.name] = {}
         tc = np.array([mean_s[k] for k in cal])
         ta = np.array([mean_s[k] for k in app])
-        rep = {}
-        try:
-            p_ref, st_ref = m.fit_cpu(fc, tc, scale=True)
-            rep["reference_fit"] = dict(_errors(wl, app, m.predict_cpu(p_ref, app), ta),
-                                        fit=st_ref, calibration_geomean_rel_error=_cal_err(
-                                            m, p_ref, cal, tc))
-        except Exception as e:  # a fit failure is reported, not hidden
-            rep["reference_fit"] = {"error": str(e)}
-        if dev is not None:
-            from paper_1904_09538_b200.device import fit_lm_batched
-            # K17 in ordered mode: the reference fit (output-scaled rows, the
-            # reference's start and LM trajectory) run on the GPU
+        for mname, text in wl.models.items():
+            m = host.HostModel(text)
+            feats = m.feature_table(cal + app)
+            fc = feats[: len(cal)]
+            rep = {}
+            p_ref = None
             try:
-                fs, ts = fc / tc[:, None], np.ones_like(tc)
                 t0 = time.perf_counter()
-                pr, sr = fit_lm_batched(dev, m, fs, ts, m.initial_point(fs, ts, scale=0)[None], mode=0)
-                dt = time.perf_counter() - t0
-                g = dict(_errors(wl, app, m.predict_cpu(pr[0], app), ta), fit=sr[0],
-                         seconds=round(dt, 4),
-                         params={n: float(v) for n, v in zip(m.params, pr[0])},
-                         calibration_geomean_rel_error=_cal_err(m, pr[0], cal, tc))
-                if "reference_fit" in rep and "error" not in rep["reference_fit"]:
-                    den = np.maximum(np.abs(p_ref), 1e-300)
-                    g["max_rel_param_diff_vs_cpu"] = float(np.max(np.abs(pr[0] - p_ref) / den))
-                rep["gpu_reference_fit"] = g
-            except Exception as e:
-                rep["gpu_reference_fit"] = {"error": str(e)}
+                p_ref, st_ref = m.fit_cpu(fc, tc, scale=True)
+                cpu_fit_s += time.perf_counter() - t0
+                cpu_fits += 1
+                rep["reference_fit"] = dict(_errors(wl, app, m.predict_cpu(p_ref, app), ta),
+                                            fit=st_ref, calibration_geomean_rel_error=_cal_err(
+                                                m, p_ref, cal, tc))
+            except Exception as e:  # a fit failure is reported, not hidden
+                rep["reference_fit"] = {"error": str(e)}
+            out[wl.name][mname] = rep
+            prep[(wl.name, mname)] = (m, p_ref, tc, ta, cal, app)
+            if dev is None:
+                continue
+            fs, ts = fc / tc[:, None], np.ones_like(tc)
+            jobs.append({"model": m, "features": fs, "t": ts,
+                         "starts": m.initial_point(fs, ts, scale=0)[None], "mode": 0})
+            where.append((wl, mname, "gpu_reference_fit"))
             p0 = m.initial_point(fc, tc, scale=2)  # relative-residual QR start
             starts = [p0]
             edges = [i for i, c in enumerate(m.cost_params) if not c]  # tanh-only params
-            if edges:
-                for e in (3.0, 10.0, 30.0, 100.0, 300.0, 1000.0):
-                    s = p0.copy()
-                    s[edges] = e
-                    starts.append(s)
-            starts = np.stack(starts)
-            t0 = time.perf_counter()
-            # mode 1|4|8: equilibrated columns, residuals relative to t
-            # (weights 1/t), forward-mode derivatives on the device
+            for e in (EDGE_STARTS if edges else ()):
+                s_ = p0.copy()
+                s_[edges] = e
+                starts.append(s_)
+            # mode 1|2|4: equilibrated columns, warp-shuffle sums, residuals
+            # relative to t (weights 1/t)
+            jobs.append({"model": m, "features": fc, "t": tc, "starts": np.stack(starts),
+                         "mode": 7})
+            where.append((wl, mname, "gpu_multistart_fit"))
+    k17 = None
+    if dev is not None and jobs:
+        from paper_1904_09538_b200.device import fit_lm_jobs
+        t0 = time.perf_counter()
+        try:
+            results, ksec = fit_lm_jobs(dev, jobs)
+        except Exception as e:  # reported, not hidden
+            for wl, mname, key in where:
+                out[wl.name][mname][key] = {"error": str(e)}
+            return out, {"error": str(e)}
+        wall = time.perf_counter() - t0
+        nfits = sum(len(j["starts"]) for j in jobs)
+        iters = sum(s["iterations"] for _, st in results for s in st)
+        k17 = {"jobs": len(jobs), "fits": nfits, "launches": 1, "kernel_s": round(ksec, 5),
+               "wall_s": round(wall, 4), "fits_per_s": round(nfits / ksec, 1),
+               "lm_iterations": iters, "iterations_per_s": round(iters / ksec, 1),
+               # the same reference-mode problems through fit_model on one host
+               # thread (the port, bit-exact with the reference)
+               "cpu_reference_fits": cpu_fits, "cpu_reference_fit_s": round(cpu_fit_s, 4)}
+        for (wl, mname, key), (params, stats) in zip(where, results):
+            m, p_ref, tc, ta, cal, app = prep[(wl.name, mname)]
+            ok = [i for i, s_ in enumerate(stats) if s_["status"] == 0]
+            best = min(ok, key=lambda i: stats[i]["residual_norm"]) if ok else 0
             try:
-                params, stats = fit_lm_batched(dev, m, fc, tc, starts, mode=13)
-                dt = time.perf_counter() - t0
-                ok = [i for i, s in enumerate(stats) if s["status"] == 0]
-                best = min(ok, key=lambda i: stats[i]["residual_norm"]) if ok else 0
-                rep["gpu_multistart_fit"] = dict(
-                    _errors(wl, app, m.predict_cpu(params[best], app), ta),
-                    fit=stats[best], starts=len(starts), seconds=round(dt, 4),
-                    calibration_geomean_rel_error=_cal_err(m, params[best], cal, tc),
-                    params={n: float(v) for n, v in zip(m.params, params[best])})
+                g = dict(_errors(wl, app, m.predict_cpu(params[best], app), ta), fit=stats[best],
+                         starts=len(stats),
+                         calibration_geomean_rel_error=_cal_err(m, params[best], cal, tc),
+                         params={n: float(v) for n, v in zip(m.params, params[best])})
+                if key == "gpu_reference_fit" and p_ref is not None:
+                    den = np.maximum(np.abs(p_ref), 1e-300)
+                    g["max_rel_param_diff_vs_cpu"] = float(np.max(np.abs(params[0] - p_ref) / den))
+                out[wl.name][mname][key] = g
             except Exception as e:  # e.g. a fit whose predictions go negative
-                rep["gpu_multistart_fit"] = {"error": str(e)}
-        out[mname] = rep
-    return out
+                out[wl.name][mname][key] = {"error": str(e)}
+    return out, k17
+
+
+def model_report(wl, cal, app, mean_s: dict[str, float], dev=None) -> dict:
+    """model_reports for one workload."""
+    return model_reports([(wl, cal, app)], mean_s, dev)[0][wl.name]
 
 
 # ---------------------------------------------------------------------------
@@ -1087,10 +1119,10 @@ def run_ours(args, dist: Dist) -> None:
                 m, kept = summarize(ts)
                 f.write(f"{kernels[k]},,{m!r},{kept},{' '.join(repr(x) for x in ts)}\n")
     # the fit runs once (rank 0); its headline parameters go to every rank
-    models, heads = {}, {}
+    models, heads, k17 = {}, {}, None
     if dist.rank == 0:
+        models, k17 = model_reports(parts, mean_s, dev)
         for wl, cal, app in parts:
-            models[wl.name] = model_report(wl, cal, app, mean_s, dev)
             forced = args.headline_model if args.headline_model in wl.models else ""
             hmodel, hfit, head = headline(models[wl.name], forced)
             if hmodel is None:  # no candidate fitted: fall back to the workload default
@@ -1148,7 +1180,7 @@ def run_ours(args, dist: Dist) -> None:
                "sample": sample_note(sample, args.workload)}
     ref_lib = reference_model_sample() if dist.world == 1 else None
     detail = {
-        "models": models, "headline": heads, "model_eval": model_eval,
+        "models": models, "headline": heads, "k17": k17, "model_eval": model_eval,
         "overlap_diagnosis": diagnosis, "paper_selection": paper,
         "tensor_variant": tensor_variant,
         "roofline": roofline, "roofline_hbm": roofline_hbm, "suite_rooflines": suite_rooflines,
@@ -1209,6 +1241,9 @@ def run_ours(args, dist: Dist) -> None:
         "model_eval": {k: me.get(k) for k in ("evaluations", "gpu_evals_per_s",
                                               "gpu_e2e_evals_per_s", "argmin_mismatches_vs_cpu",
                                               "reference_predict_evals_per_s")} if me else None,
+        "k17": ({k: k17.get(k) for k in ("fits", "launches", "kernel_s", "fits_per_s",
+                                          "cpu_reference_fits", "cpu_reference_fit_s")}
+                if k17 and "error" not in k17 else k17),
         "gpu_launches": e2e_launch_total,
         "clocks": {k: clocks.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons")},
         "detail": detail_ref,

@@ -245,6 +245,26 @@ int ps_fit_lm_batched_ex(ps_ctx* ctx, const ps_bytecode* model, const ps_bytecod
                          const ps_fit_opts* opts, int mode, double* params_inout,
                          ps_fit_stats* stats);
 
+/* K17 v2: every fit of a calibration round in one launch. A job is one model
+ * (model file text: output id line + expression, model.cpp:625-644) fitted
+ * from nbatch starts to nr rows; the library compiles the model and its
+ * derivatives into one straight-line program with shared subexpressions.
+ * mode bits: 1 column equilibration, 2 warp-shuffle sums (default: row-order
+ * sums, bit-identical to fit_model), 4 residuals relative to t.
+ * shared_rows = 1: features [nr][nf] and t [nr] are shared by every start
+ * (else [nbatch][nr][nf], [nbatch][nr]). Host buffers; kernel_seconds (may
+ * be NULL) is the device time of the one launch. */
+typedef struct ps_lm_job {
+  const char* model_text;
+  int32_t nf, nr, nbatch, mode, shared_rows, reserved;
+  const double* features;
+  const double* t;
+  ps_fit_opts opts;
+  double* params_inout;   /* [nbatch][np] */
+  ps_fit_stats* stats;    /* [nbatch] */
+} ps_lm_job;
+int ps_fit_lm_jobs(ps_ctx* ctx, int njobs, const ps_lm_job* jobs, double* kernel_seconds);
+
 /* The device tanh K17 and K18 evaluate sstep/tanh with (csrc/cuda/libm_glibc.cuh):
  * the host glibc's std::tanh (model.cpp:253) restated bit for bit, so device
  * and reference model evaluations agree exactly. x, out: n host doubles. */
@@ -313,6 +333,13 @@ int ps_model_bytecode(const char* model_text, int which, int32_t* ops, int cap_o
  * brute_force_count), 2 = the same enumeration on the GPU of ctx. */
 int ps_enumerate(ps_ctx* ctx, const char* variant_id, int mode, char* out, size_t cap,
                  size_t* needed);
+/* The model (and with_jacobian, its np symbolic derivatives, diff_expr
+ * model.cpp:289-330) as one straight-line register program with common
+ * subexpressions computed once (what K17/K18 execute): JSON {"insns": [op <<
+ * 16 | dst, a << 16 | b, ...], "consts", "outputs": [slot per expression],
+ * "n_slots", "n_nodes"}. */
+int ps_model_program(const char* model_text, int with_jacobian, char* out, size_t cap,
+                     size_t* needed);
 /* Process-wide options: "partial_subgroups" = strict (the reference: raise
  * when a work-group is not a whole number of sub-groups) | round_up
  * (ceil(wg/32) sub-groups); "launch_geometry" = realised

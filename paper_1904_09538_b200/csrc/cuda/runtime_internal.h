@@ -122,6 +122,25 @@ int bytecode_depth(const int32_t* ops, int n_ops, int n_consts, int np, int nf);
 void set_literal_geometry(bool on);
 bool literal_geometry();
 
+// K17 v2 (lm_jobs.cu): straight-line model programs (host-compiled,
+// perfseer::compile_program) and one fit job per (model, problem, starts).
+struct LmProgramHost {
+  const uint32_t* insns;  // [n_insns][2]
+  const double* consts;
+  const int32_t* outputs;
+  int n_insns, n_consts, n_outputs, n_slots;
+};
+struct LmJobHost {
+  LmProgramHost value, full;  // value: the model; full: the model and its np derivatives
+  int np, nf, nr, nbatch, mode, shared_rows;
+  const double* features;  // [shared_rows ? 1 : nbatch][nr][nf]
+  const double* t;         // [shared_rows ? 1 : nbatch][nr]
+  ps_fit_opts opts;
+  double* params;          // [nbatch][np] in/out
+  ps_fit_stats* stats;     // [nbatch]
+};
+int fit_lm_jobs_gpu(Ctx* c, int njobs, const LmJobHost* jobs, double* kernel_seconds);
+
 int eval_tables_gpu(Ctx* c, const FlatTables& t, const int64_t* points, int64_t npts, double* pred,
                     uint8_t* argmin, double* kernel_seconds);
 

@@ -208,6 +208,64 @@ int ps_model_bytecode(const char* model_text, int which, int32_t* ops, int cap_o
   });
 }
 
+int ps_model_program(const char* model_text, int with_jacobian, char* out, size_t cap, size_t* needed) {
+  return guarded([&] {
+    Model m = model_from_text(model_text);
+    Program pr = compile_model_program(m, with_jacobian != 0);
+    nlohmann::json j;
+    j["insns"] = pr.insns;
+    j["consts"] = pr.consts;
+    j["outputs"] = pr.outputs;
+    j["n_slots"] = pr.n_slots;
+    j["n_nodes"] = pr.n_nodes;
+    return copy_out(j.dump(), out, cap, needed);
+  });
+}
+
+int ps_fit_lm_jobs(ps_ctx* ctx, int njobs, const ps_lm_job* jobs, double* kernel_seconds) {
+  return guarded([&] {
+    if (!ctx || !jobs || njobs < 1) throw EvalError("ps_fit_lm_jobs: bad argument");
+    // one value program and one value+Jacobian program per distinct model text
+    std::map<std::string, std::pair<Program, Program>> progs;
+    std::vector<ps::LmJobHost> hj(static_cast<size_t>(njobs));
+    for (int j = 0; j < njobs; ++j) {
+      const ps_lm_job& in = jobs[j];
+      if (!in.model_text || !in.features || !in.t || !in.params_inout || !in.stats)
+        throw EvalError("ps_fit_lm_jobs: job " + std::to_string(j) + " has a null pointer");
+      auto it = progs.find(in.model_text);
+      if (it == progs.end()) {
+        Model m = model_from_text(in.model_text);
+        if (int(m.features.size()) != in.nf)
+          throw EvalError("ps_fit_lm_jobs: job " + std::to_string(j) + ": model has " +
+                          std::to_string(m.features.size()) + " features, job gives " + std::to_string(in.nf));
+        it = progs.emplace(in.model_text, std::make_pair(compile_model_program(m, false),
+                                                         compile_model_program(m, true))).first;
+      }
+      auto view = [](const Program& pr) {
+        return ps::LmProgramHost{pr.insns.data(), pr.consts.data(), pr.outputs.data(), int(pr.insns.size() / 2),
+                                 int(pr.consts.size()), int(pr.outputs.size()), pr.n_slots};
+      };
+      ps::LmJobHost& h = hj[size_t(j)];
+      h.value = view(it->second.first);
+      h.full = view(it->second.second);
+      h.np = int(it->second.second.outputs.size()) - 1;
+      h.nf = in.nf;
+      h.nr = in.nr;
+      h.nbatch = in.nbatch;
+      h.mode = in.mode;
+      h.shared_rows = in.shared_rows;
+      h.features = in.features;
+      h.t = in.t;
+      h.opts = in.opts;
+      h.params = in.params_inout;
+      h.stats = in.stats;
+    }
+    const int rc = ps::fit_lm_jobs_gpu(reinterpret_cast<ps::Ctx*>(ctx), njobs, hj.data(), kernel_seconds);
+    if (rc) throw EvalError(ps_last_error());
+    return PS_OK;
+  });
+}
+
 int ps_set_option(const char* key, const char* value) {
   return guarded([&] {
     const std::string k = key ? key : "", v = value ? value : "";

@@ -221,3 +221,46 @@ def fit_lm_batched(dev: CudaDevice, model, features: np.ndarray, t: np.ndarray, 
                                  C.byref(o), mode, dptr(params), stats))
     return params, [{"residual_norm": s.residual_norm, "iterations": s.iterations,
                      "converged": bool(s.converged), "status": s.status} for s in stats]
+
+
+class LmJob(C.Structure):
+    """ps_lm_job (include/perfseer_b200.h)."""
+    _fields_ = [("model_text", C.c_char_p), ("nf", C.c_int32), ("nr", C.c_int32),
+                ("nbatch", C.c_int32), ("mode", C.c_int32), ("shared_rows", C.c_int32),
+                ("reserved", C.c_int32), ("features", C.POINTER(C.c_double)),
+                ("t", C.POINTER(C.c_double)), ("opts", _abi.FitOpts),
+                ("params_inout", C.POINTER(C.c_double)), ("stats", C.POINTER(_abi.FitStats))]
+
+
+def fit_lm_jobs(dev: CudaDevice, jobs: list[dict]):
+    """K17 v2: every fit in ONE launch (ps_fit_lm_jobs). Each job: {"model":
+    HostModel, "features": [nr, nf], "t": [nr], "starts": [nbatch, np],
+    "mode": bits (1 equilibrate, 2 shuffle sums, 4 relative residuals),
+    "opts": FitOpts or None}. Returns ([(params [nbatch, np], stats list)],
+    kernel seconds)."""
+    from ._abi import FitStats
+    from .host import default_fit_opts
+    L = lib()
+    if not getattr(L, "_lm_jobs_declared", False):
+        L.ps_fit_lm_jobs.argtypes = [C.c_void_p, C.c_int, C.POINTER(LmJob), C.POINTER(C.c_double)]
+        L.ps_fit_lm_jobs.restype = C.c_int
+        L._lm_jobs_declared = True
+    keep, arr, outs = [], (LmJob * len(jobs))(), []
+    dptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    for j, job in enumerate(jobs):
+        m = job["model"]
+        f = np.ascontiguousarray(job["features"], dtype=np.float64)
+        t = np.ascontiguousarray(job["t"], dtype=np.float64)
+        p = np.ascontiguousarray(np.atleast_2d(job["starts"]), dtype=np.float64).copy()
+        st = (FitStats * p.shape[0])()
+        text = m.text.encode()
+        keep += [f, t, p, st, text]
+        arr[j] = LmJob(text, f.shape[1], f.shape[0], p.shape[0], int(job.get("mode", 0)), 1, 0,
+                       dptr(f), dptr(t), job.get("opts") or default_fit_opts(), dptr(p), st)
+        outs.append((p, st))
+    secs = C.c_double()
+    check(L.ps_fit_lm_jobs(dev._ctx, len(jobs), arr, C.byref(secs)))
+    res = [(p, [{"residual_norm": s.residual_norm, "iterations": s.iterations,
+                 "converged": bool(s.converged), "status": s.status} for s in st])
+           for p, st in outs]
+    return res, secs.value

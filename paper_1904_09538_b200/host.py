@@ -21,6 +21,8 @@ def _declare() -> C.CDLL:
     L.ps_model_info.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, _P(C.c_size_t)]
     L.ps_kernel_json.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, _P(C.c_size_t)]
     L.ps_kernel_json.restype = C.c_int
+    L.ps_model_program.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_size_t, _P(C.c_size_t)]
+    L.ps_model_program.restype = C.c_int
     L.ps_feature_table.argtypes = [C.c_char_p, C.c_char_p, C.c_int, _P(C.c_double), C.c_int64]
     L.ps_fit_cpu.argtypes = [C.c_char_p, _P(C.c_double), _P(C.c_double), C.c_int, C.c_int,
                              _P(FitOpts), _P(C.c_double), _P(FitStats)]
@@ -123,6 +125,11 @@ class HostModel:
                                         "\n".join(variant_ids).encode(), sub_group_size,
                                         _dptr(out), out.size))
         return out
+
+    def program(self, with_jacobian: bool = True) -> dict:
+        """The CSE'd straight-line program K17/K18 run (ps_model_program)."""
+        return json.loads(_string_call(_declare().ps_model_program, self.text.encode(),
+                                       int(with_jacobian)))
 
     def bytecode(self, which: int = -1):
         cap = 1 << 14

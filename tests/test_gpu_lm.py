@@ -165,3 +165,55 @@ def test_lm_rejects_programs_deeper_than_the_device_stack(dev):
     assert rc != 0 and b"stack" in L.ps_last_error()
     with pytest.raises(PsError):
         check(rc)
+
+
+def test_lm_jobs_one_launch_reference_mode_bitwise(dev):
+    """K17 v2 (ps_fit_lm_jobs): every model of every workload on the r01
+    table in ONE launch, reference mode: bit-identical to fit_model."""
+    import bench
+    from paper_1904_09538_b200 import host, workloads
+    from paper_1904_09538_b200.device import fit_lm_jobs
+    jobs, refs = [], []
+    for wname, mname in _CASES:
+        parts, _ = bench.workload_kernels(wname)
+        wl, cal, _app = parts[0]
+        cal = [k for k in cal if k in _ROWS]
+        m = host.HostModel(wl.models[mname])
+        fc = m.feature_table(cal)
+        tc = np.array([_ROWS[k] for k in cal])
+        try:
+            p_ref, st = m.fit_cpu(fc, tc, scale=True)
+        except Exception:
+            continue
+        fs = fc / tc[:, None]
+        jobs.append({"model": m, "features": fs, "t": np.ones_like(tc),
+                     "starts": m.initial_point(fs, np.ones_like(tc), scale=0)[None], "mode": 0})
+        refs.append((f"{wname}-{mname}", p_ref, st))
+    res, secs = fit_lm_jobs(dev, jobs)
+    assert secs > 0
+    for (name, p_ref, st), (pg, sg) in zip(refs, res):
+        assert sg[0]["iterations"] == st["iterations"], name
+        np.testing.assert_array_equal(pg[0], p_ref, err_msg=name)
+
+
+@pytest.mark.parametrize("case", FITS, ids=lambda c: c["name"])
+def test_lm_jobs_golden_fits(dev, case):
+    from paper_1904_09538_b200.device import fit_lm_jobs
+    m, F, t = _problem(case)
+    p0 = m.initial_point(F, t, scale=False)
+    (params, stats), = fit_lm_jobs(dev, [{"model": m, "features": F, "t": t, "starts": p0[None],
+                                          "mode": 0}])[0]
+    ref = np.array(case["params"])
+    assert stats[0]["iterations"] == case["iterations"] or not case["converged"]
+    np.testing.assert_allclose(params[0], ref, rtol=1e-4, atol=1e-12 * np.abs(ref).max())
+
+
+def test_lm_jobs_multistart_shuffle_matches_single_starts(dev):
+    from paper_1904_09538_b200.device import fit_lm_jobs
+    case = next(c for c in FITS if c["name"] == "overlap_seed5")
+    m, F, t = _problem(case)
+    p0 = m.initial_point(F, t, scale=False)
+    starts = np.stack([p0] + [np.where(np.array(m.params) == "p_edge", e, p0) for e in (3.0, 10.0)])
+    res, _ = fit_lm_jobs(dev, [{"model": m, "features": F, "t": t, "starts": starts, "mode": 7},
+                               {"model": m, "features": F, "t": t, "starts": starts[1:2], "mode": 7}])
+    np.testing.assert_array_equal(res[0][0][1], res[1][0][0])
