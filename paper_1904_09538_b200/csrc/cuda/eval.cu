@@ -24,28 +24,29 @@ struct DevTables {
   FlatTables t;  // pointers are device pointers
 };
 
-__device__ double eval_model_bc(const int32_t* ops, int n_ops, const double* consts, const double* p,
-                                const double* f) {
-  double st[kEvalMaxStack];
-  int sp = 0;
-  for (int i = 0; i < n_ops; ++i) {
-    const int32_t w = ops[i];
-    const int code = w >> 16, arg = w & 0xffff;
-    switch (code) {
-      case PS_BC_NUM: st[sp++] = consts[arg]; break;
-      case PS_BC_PARAM: st[sp++] = p[arg]; break;
-      case PS_BC_FEAT: st[sp++] = f[arg]; break;
-      case PS_BC_TANH: st[sp - 1] = glibc_tanh(st[sp - 1]); break;
-      default: {
-        const double b = st[--sp], a = st[sp - 1];
-        st[sp - 1] = code == PS_BC_ADD ? __dadd_rn(a, b)
-                     : code == PS_BC_SUB ? __dsub_rn(a, b)
-                     : code == PS_BC_MUL ? __dmul_rn(a, b)
-                                         : __ddiv_rn(a, b);
-      }
+// The model's straight-line register program (common subexpressions once,
+// ps_model.cpp compile_program): the same IEEE operations on the same
+// operands as eval_model's tree walk, so the same bits.
+__device__ double eval_model_prog(const uint32_t* __restrict__ insns, int n, const double* __restrict__ consts,
+                                  const double* __restrict__ p, const double* f, int out) {
+  double s[kEvalMaxRegs];
+  for (int i = 0; i < n; ++i) {
+    const uint32_t w0 = __ldg(insns + 2 * i), w1 = __ldg(insns + 2 * i + 1);
+    const int op = int(w0 >> 16), d = int(w0 & 0xffff), a = int(w1 >> 16), b = int(w1 & 0xffff);
+    double v;
+    switch (op) {
+      case PS_BC_NUM: v = __ldg(consts + a); break;
+      case PS_BC_PARAM: v = __ldg(p + a); break;
+      case PS_BC_FEAT: v = f[a]; break;
+      case PS_BC_TANH: v = glibc_tanh(s[a]); break;
+      case PS_BC_ADD: v = __dadd_rn(s[a], s[b]); break;
+      case PS_BC_SUB: v = __dsub_rn(s[a], s[b]); break;
+      case PS_BC_MUL: v = __dmul_rn(s[a], s[b]); break;
+      default: v = __ddiv_rn(s[a], s[b]);
     }
+    s[d] = v;
   }
-  return st[0];
+  return s[out];
 }
 
 __global__ void __launch_bounds__(128) eval_points_kernel(FlatTables t, const int64_t* __restrict__ points,
@@ -91,8 +92,10 @@ __global__ void __launch_bounds__(128) eval_points_kernel(FlatTables t, const in
                          : (double)acc / (double)den;
         }
       }
-      const double y = eval_model_bc(t.ops + t.model_op_begin[m], t.model_op_begin[m + 1] - t.model_op_begin[m],
-                                     t.consts + t.model_const_begin[m], t.params + t.model_param_begin[m], f);
+      const double y = eval_model_prog(t.insns + 2 * (size_t)t.model_insn_begin[m],
+                                       t.model_insn_begin[m + 1] - t.model_insn_begin[m],
+                                       t.consts + t.model_const_begin[m], t.params + t.model_param_begin[m], f,
+                                       t.model_out[m]);
       pred[pt * t.nvar + v] = y;
       const int g = t.var_group[v];
       if (besti[g] < 0 || y < best[g]) {
@@ -110,13 +113,9 @@ int eval_tables_gpu(Ctx* c, const FlatTables& h, const int64_t* points, int64_t 
   if (h.nvar > kEvalMaxVariants) return set_error(PS_ERR_ARG, "at most %d variants", kEvalMaxVariants);
   for (int m = 0; m < h.nmodels; ++m) {
     if (h.model_nf[m] > kEvalMaxFeat) return set_error(PS_ERR_ARG, "model with more than %d features", kEvalMaxFeat);
-    const int np = h.model_param_begin[m + 1] - h.model_param_begin[m];
-    const int depth = bytecode_depth(h.ops + h.model_op_begin[m], h.model_op_begin[m + 1] - h.model_op_begin[m],
-                                     h.model_const_begin[m + 1] - h.model_const_begin[m], np, h.model_nf[m]);
-    if (depth < 0) return set_error(PS_ERR_ARG, "model %d: malformed bytecode", m);
-    if (depth > kEvalMaxStack)
-      return set_error(PS_ERR_ARG, "model %d: expression needs a stack of %d (device evaluator: %d)", m, depth,
-                       kEvalMaxStack);
+    if (h.model_regs[m] > kEvalMaxRegs)
+      return set_error(PS_ERR_ARG, "model %d: program needs %d registers (device evaluator: %d)", m,
+                       h.model_regs[m], kEvalMaxRegs);
   }
   if (cudaSetDevice(c->device) != cudaSuccess) return set_error(PS_ERR_CUDA, "cudaSetDevice failed");
   // Pack every table array into one device allocation.
@@ -136,8 +135,10 @@ int eval_tables_gpu(Ctx* c, const FlatTables& h, const int64_t* points, int64_t 
       {h.term_coef, sizeof(int64_t) * h.nterms, (void**)&d.term_coef},
       {h.term_exp, (size_t)4 * h.nterms, (void**)&d.term_exp},
       {h.model_nf, sizeof(int32_t) * h.nmodels, (void**)&d.model_nf},
-      {h.model_op_begin, sizeof(int32_t) * (h.nmodels + 1), (void**)&d.model_op_begin},
-      {h.ops, sizeof(int32_t) * h.model_op_begin[h.nmodels], (void**)&d.ops},
+      {h.model_insn_begin, sizeof(int32_t) * (h.nmodels + 1), (void**)&d.model_insn_begin},
+      {h.insns, sizeof(uint32_t) * 2 * (size_t)h.model_insn_begin[h.nmodels], (void**)&d.insns},
+      {h.model_out, sizeof(int32_t) * h.nmodels, (void**)&d.model_out},
+      {h.model_regs, sizeof(int32_t) * h.nmodels, (void**)&d.model_regs},
       {h.model_const_begin, sizeof(int32_t) * (h.nmodels + 1), (void**)&d.model_const_begin},
       {h.consts, sizeof(double) * std::max(1, h.model_const_begin[h.nmodels]), (void**)&d.consts},
       {h.model_param_begin, sizeof(int32_t) * (h.nmodels + 1), (void**)&d.model_param_begin},

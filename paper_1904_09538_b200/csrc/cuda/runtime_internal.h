@@ -94,9 +94,11 @@ struct FlatTables {
   const int64_t *feat_den, *term_coef;
   const int8_t* term_exp;  // [nterms][4]
   int nslots, nterms;
-  const int32_t* model_nf;        // [nmodels]
-  const int32_t* model_op_begin;  // [nmodels + 1] into ops
-  const int32_t* ops;
+  const int32_t* model_nf;          // [nmodels]
+  const int32_t* model_insn_begin;  // [nmodels + 1] into insns (instruction index)
+  const uint32_t* insns;            // [n][2]: op << 16 | dst, a << 16 | b
+  const int32_t* model_out;         // [nmodels] result register
+  const int32_t* model_regs;        // [nmodels] registers used
   const int32_t* model_const_begin;  // [nmodels + 1] into consts
   const double* consts;
   const int32_t* model_param_begin;  // [nmodels + 1] into params
@@ -108,6 +110,7 @@ struct FlatTables {
 constexpr int kEvalMaxFeat = 48;
 constexpr int kEvalMaxGroups = 8;
 constexpr int kEvalMaxStack = 48;
+constexpr int kEvalMaxRegs = 64;
 constexpr int kEvalMaxVariants = 256;  // argmin is one byte per group
 constexpr int kLmMaxParams = 24;
 constexpr int kLmMaxStack = 48;

@@ -303,7 +303,8 @@ int ps_geo_mean_rel_error(const double* pred, const double* meas, int n, double*
 struct ps_tables {
   perfseer::VariantTables t;
   // flattened model programs for the device
-  std::vector<int32_t> model_op_begin, ops, model_const_begin, model_param_begin;
+  std::vector<int32_t> model_insn_begin, model_out, model_regs, model_const_begin, model_param_begin;
+  std::vector<uint32_t> insns;
   std::vector<double> consts, params;
   std::vector<int8_t> term_exp;
   ps::FlatTables flat() const {
@@ -322,8 +323,10 @@ struct ps_tables {
     f.nslots = int(t.feat_begin.size());
     f.nterms = int(t.term_coef.size());
     f.model_nf = t.model_nf.data();
-    f.model_op_begin = model_op_begin.data();
-    f.ops = ops.data();
+    f.model_insn_begin = model_insn_begin.data();
+    f.insns = insns.data();
+    f.model_out = model_out.data();
+    f.model_regs = model_regs.data();
     f.model_const_begin = model_const_begin.data();
     f.consts = consts.data();
     f.model_param_begin = model_param_begin.data();
@@ -344,15 +347,17 @@ int ps_tables_build(const char* spec_json, ps_tables** out) {
       delete h;
       throw;
     }
-    h->model_op_begin.push_back(0);
+    h->model_insn_begin.push_back(0);
     h->model_const_begin.push_back(0);
     h->model_param_begin.push_back(0);
     for (size_t m = 0; m < h->t.models.size(); ++m) {
-      const auto& bc = h->t.models[m];
-      h->ops.insert(h->ops.end(), bc.ops.begin(), bc.ops.end());
-      h->consts.insert(h->consts.end(), bc.consts.begin(), bc.consts.end());
+      const auto& pr = h->t.models[m];
+      h->insns.insert(h->insns.end(), pr.insns.begin(), pr.insns.end());
+      h->consts.insert(h->consts.end(), pr.consts.begin(), pr.consts.end());
       h->params.insert(h->params.end(), h->t.params[m].begin(), h->t.params[m].end());
-      h->model_op_begin.push_back(int32_t(h->ops.size()));
+      h->model_insn_begin.push_back(int32_t(h->insns.size() / 2));
+      h->model_out.push_back(pr.outputs.at(0));
+      h->model_regs.push_back(pr.n_slots);
       h->model_const_begin.push_back(int32_t(h->consts.size()));
       h->model_param_begin.push_back(int32_t(h->params.size()));
     }
@@ -397,7 +402,8 @@ int ps_eval_cpu(const ps_tables* tables, const int64_t* points, int64_t npts, do
         for (size_t v = 0; v < nvar; ++v) {
           const auto f = eval_point_cpu(t, v, points + pt * 4);
           const int m = t.var_model[v];
-          const double y = run_bytecode(t.models[size_t(m)], t.params[size_t(m)].data(), f.data());
+          double y;
+          run_program(t.models[size_t(m)], t.params[size_t(m)].data(), f.data(), &y);
           pred[pt * int64_t(nvar) + int64_t(v)] = y;
           const int g = t.var_group[v];
           if (besti[size_t(g)] < 0 || y < best[size_t(g)]) {

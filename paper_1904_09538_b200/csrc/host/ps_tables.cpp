@@ -64,7 +64,7 @@ VariantTables build_variant_tables(const std::string& spec_json) {
     if (it == model_index.end()) {
       mi = int(t.models.size());
       model_index[key] = mi;
-      t.models.push_back(compile_bytecode(m.expr));
+      t.models.push_back(compile_model_program(m, false));
       t.params.push_back(p);
       t.model_nf.push_back(int(m.features.size()));
     } else {
@@ -114,9 +114,9 @@ VariantTables build_variant_tables(const std::string& spec_json) {
   for (int g : t.var_group) t.ngroups = std::max(t.ngroups, g + 1);
   if (t.var_model.size() > 256)
     throw EvalError("at most 256 variants per table set (the argmin is one byte per group)");
-  for (const auto& bc : t.models)
-    if (bc.max_stack > 48) throw EvalError("model expression needs a stack of " + std::to_string(bc.max_stack) +
-                                           " (device evaluator: 48)");
+  for (const auto& pr : t.models)
+    if (pr.n_slots > 64) throw EvalError("model program needs " + std::to_string(pr.n_slots) +
+                                         " registers (device evaluator: 64)");
   return t;
 }
 

@@ -21,8 +21,8 @@ struct VariantTables {
   // per term: integer coefficient and exponents of point coordinates 0..3
   std::vector<int64_t> term_coef;
   std::vector<std::array<int8_t, 4>> term_exp;
-  // per model
-  std::vector<Bytecode> models;
+  // per model: the value program (CSE'd straight-line, compile_program)
+  std::vector<Program> models;
   std::vector<std::vector<double>> params;
   std::vector<int32_t> model_nf;
   int ngroups = 0;

@@ -58,16 +58,35 @@ class PredictionTables:
         except Exception:
             pass
 
-    def _out(self, points: np.ndarray):
+    def _out(self, points: np.ndarray, out=None):
         pts = np.ascontiguousarray(points, dtype=np.int64)
         if pts.ndim != 2 or pts.shape[1] != 4:
             raise ValueError("points must be [npts, 4] int64")
+        if out is not None:
+            pred, arg = out
+            if pred.shape != (pts.shape[0], self.nvar) or arg.shape != (pts.shape[0], self.ngroups):
+                raise ValueError("output buffers do not match the point count")
+            return pts, pred, arg
         pred = np.empty((pts.shape[0], self.nvar), dtype=np.float64)
         arg = np.empty((pts.shape[0], self.ngroups), dtype=np.uint8)
         return pts, pred, arg
 
-    def eval_gpu(self, dev, points: np.ndarray):
-        pts, pred, arg = self._out(points)
+    def pinned_buffers(self, npts: int):
+        """Page-locked point and result buffers (ps_host_alloc) so the
+        end-to-end path copies at PCIe speed: (points [npts, 4] int64,
+        pred [npts, nvar] float64, argmin [npts, ngroups] uint8, keep-alive)."""
+        from .device import PinnedArray
+        bufs = [PinnedArray(max(1, npts * 4 * 8)), PinnedArray(max(1, npts * self.nvar * 8)),
+                PinnedArray(max(1, npts * self.ngroups))]
+        pts = bufs[0].numpy(np.int64)[: npts * 4].reshape(npts, 4)
+        pred = bufs[1].numpy(np.float64)[: npts * self.nvar].reshape(npts, self.nvar)
+        arg = bufs[2].numpy(np.uint8)[: npts * self.ngroups].reshape(npts, self.ngroups)
+        return pts, pred, arg, bufs
+
+    def eval_gpu(self, dev, points: np.ndarray, out=None):
+        """K18 on dev. out = (pred, argmin) writes into caller buffers (e.g.
+        from pinned_buffers) instead of fresh pageable arrays."""
+        pts, pred, arg = self._out(points, out)
         secs = C.c_double()
         check(_declare().ps_eval_batched(dev._ctx, self._h, pts.ctypes.data_as(_P(C.c_int64)),
                                          pts.shape[0], pred.ctypes.data_as(_P(C.c_double)),

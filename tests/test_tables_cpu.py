@@ -76,8 +76,8 @@ def test_tables_reject_models_deeper_than_the_device_stack():
     from paper_1904_09538_b200 import PsError
     from paper_1904_09538_b200.predict import PredictionTables
     v = _variants("linear")[0]
-    # a right-nested sum of 50 terms needs a 50-deep postfix stack
-    terms = " + (".join(f"p_{i} * f_thread_groups" for i in range(50)) + ")" * 49
+    # a right-nested sum of 80 distinct terms keeps ~80 partial values live
+    terms = " + (".join(f"p_{i} * f_thread_groups" for i in range(80)) + ")" * 79
     text = "f_exec_wall_time_x\n" + terms + "\n"
-    with pytest.raises(PsError, match="stack"):
-        PredictionTables([dict(v, model=text, params=[1e-12] * 50)])
+    with pytest.raises(PsError, match="registers"):
+        PredictionTables([dict(v, model=text, params=[1e-12] * 80)])
