@@ -437,8 +437,8 @@ int fit_lm_jobs_gpu(Ctx* c, int njobs, const LmJobHost* jobs, double* kernel_sec
   }
   DevJob* djobs = static_cast<DevJob*>(up(dj.data(), sizeof(DevJob) * njobs));
   const size_t dyn = rows_in_smem ? rows_bytes : 0;
-  if (dyn > 48 * 1024 &&
-      cudaFuncSetAttribute(lm_jobs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess)
+  // static + dynamic above 48 KB needs the opt-in limit raised
+  if (cudaFuncSetAttribute(lm_jobs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess)
     return set_error(PS_ERR_CUDA, "LM jobs: cannot reserve %zu B of shared memory", dyn);
   if ((rc = events(c, 2))) return rc;
   cudaEventRecord(c->ev[0], c->stream);
