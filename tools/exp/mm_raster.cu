@@ -151,8 +151,15 @@ int main(int argc, char** argv) {
       float g128 = time([&] { nopf_p<128><<<grid, block>>>(a, b, c, n, 16); }, reps);
       float g256 = time([&] { nopf_p<256><<<grid, block>>>(a, b, c, n, 16); }, reps);
       printf("n %d product-style raster GM0 %.3f  GM64 %.3f  GM128 %.3f  GM256 %.3f ms\n", n, g0, g64, g128, g256);
+      // group heights dividing the SM count (148 = 4 x 37): CTAs s, s+148, ...
+      // of a wave share a block row (and its a rows in L1) when CTAs are
+      // dealt to SMs in id order, while each group streams b from L2 once
+      float g37 = time([&] { nopf_p<37><<<grid, block>>>(a, b, c, n, 16); }, reps);
+      float g74 = time([&] { nopf_p<74><<<grid, block>>>(a, b, c, n, 16); }, reps);
+      float g148 = time([&] { nopf_p<148><<<grid, block>>>(a, b, c, n, 16); }, reps);
+      printf("n %d product-style raster GM37 %.3f  GM74 %.3f  GM148 %.3f ms\n", n, g37, g74, g148);
     }
-    for (int GM : {0, 128}) {
+    for (int GM : {0, 37, 74, 128, 148}) {
       float tn = time([&] { nopf_r<<<grid, block>>>(a, b, c, n, GM); }, reps);
       cudaMemcpy(r1.data(), c, N * 4, cudaMemcpyDeviceToHost);
       bool same = memcmp(r0.data(), r1.data(), N * 4) == 0;
