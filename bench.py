@@ -371,7 +371,7 @@ def model_reports(parts, mean_s: dict[str, float], dev=None) -> tuple[dict, dict
     out: dict = {}
     jobs, where = [], []
     prep = {}
-    cpu_fit_s, cpu_fits = 0.0, 0
+    problems = []
     for wl, cal, app in parts:
         out[wl.name] = {}
         tc = np.array([mean_s[k] for k in cal])
@@ -382,18 +382,21 @@ def model_reports(parts, mean_s: dict[str, float], dev=None) -> tuple[dict, dict
             fc = feats[: len(cal)]
             rep = {}
             p_ref = None
-            try:
-                t0 = time.perf_counter()
-                p_ref, st_ref = m.fit_cpu(fc, tc, scale=True)
-                cpu_fit_s += time.perf_counter() - t0
-                cpu_fits += 1
-                rep["reference_fit"] = dict(_errors(wl, app, m.predict_cpu(p_ref, app), ta),
-                                            fit=st_ref, calibration_geomean_rel_error=_cal_err(
-                                                m, p_ref, cal, tc))
-            except Exception as e:  # a fit failure is reported, not hidden
-                rep["reference_fit"] = {"error": str(e)}
+            if dev is None:
+                # no GPU: fit_model itself (the port, bit-exact with the
+                # reference); with a GPU the reference library runs the same
+                # problems below (reference_library_fits) and K17's
+                # reference mode reproduces it bit for bit
+                try:
+                    p_ref, st_ref = m.fit_cpu(fc, tc, scale=True)
+                    rep["reference_fit"] = dict(_errors(wl, app, m.predict_cpu(p_ref, app), ta),
+                                                fit=st_ref, calibration_geomean_rel_error=_cal_err(
+                                                    m, p_ref, cal, tc))
+                except Exception as e:  # a fit failure is reported, not hidden
+                    rep["reference_fit"] = {"error": str(e)}
             out[wl.name][mname] = rep
             prep[(wl.name, mname)] = (m, p_ref, tc, ta, cal, app)
+            problems.append({"model": text, "features": fc.tolist(), "t": tc.tolist(), "scale": True})
             if dev is None:
                 continue
             fs, ts = fc / tc[:, None], np.ones_like(tc)
@@ -427,10 +430,7 @@ def model_reports(parts, mean_s: dict[str, float], dev=None) -> tuple[dict, dict
         iters = sum(s["iterations"] for _, st in results for s in st)
         k17 = {"jobs": len(jobs), "fits": nfits, "launches": 1, "kernel_s": round(ksec, 5),
                "wall_s": round(wall, 4), "fits_per_s": round(nfits / ksec, 1),
-               "lm_iterations": iters, "iterations_per_s": round(iters / ksec, 1),
-               # the same reference-mode problems through fit_model on one host
-               # thread (the port, bit-exact with the reference)
-               "cpu_reference_fits": cpu_fits, "cpu_reference_fit_s": round(cpu_fit_s, 4)}
+               "lm_iterations": iters, "iterations_per_s": round(iters / ksec, 1)}
         for (wl, mname, key), (params, stats) in zip(where, results):
             m, p_ref, tc, ta, cal, app = prep[(wl.name, mname)]
             ok = [i for i, s_ in enumerate(stats) if s_["status"] == 0]
@@ -440,13 +440,58 @@ def model_reports(parts, mean_s: dict[str, float], dev=None) -> tuple[dict, dict
                          starts=len(stats),
                          calibration_geomean_rel_error=_cal_err(m, params[best], cal, tc),
                          params={n: float(v) for n, v in zip(m.params, params[best])})
-                if key == "gpu_reference_fit" and p_ref is not None:
-                    den = np.maximum(np.abs(p_ref), 1e-300)
-                    g["max_rel_param_diff_vs_cpu"] = float(np.max(np.abs(params[0] - p_ref) / den))
                 out[wl.name][mname][key] = g
             except Exception as e:  # e.g. a fit whose predictions go negative
                 out[wl.name][mname][key] = {"error": str(e)}
+        # the reference library itself on the same reference-mode problems:
+        # the CPU baseline of K17 and a bitwise pin of its reference mode
+        ref = reference_library_fits(problems)
+        if "params_hex" in ref:
+            same = total = 0
+            for (wl, mname, key), (params, _st), got in zip(
+                    [w for w in where if w[2] == "gpu_reference_fit"],
+                    [r for w, r in zip(where, results) if w[2] == "gpu_reference_fit"],
+                    ref["params_hex"]):
+                total += 1
+                rec = out[wl.name][mname]["gpu_reference_fit"]
+                if isinstance(got, str):  # the reference raises (e.g. divergence)
+                    rec["reference_library"] = {"error": got}
+                    continue
+                want = np.array([int(h, 16) for h in got], dtype=np.uint64).view(np.float64)
+                eq = bool(np.array_equal(params[0].view(np.uint64), want.view(np.uint64)))
+                same += eq
+                den = np.maximum(np.abs(want), 1e-300)
+                rec["reference_library"] = {"bitwise_equal": eq, "max_rel_param_diff": float(
+                    np.max(np.abs(params[0] - want) / den))}
+            k17["reference_library"] = {
+                "fits": ref["fits"], "seconds_1thread": round(ref["seconds_1thread"], 3),
+                "threads": ref["threads"], "seconds_threads": round(ref["seconds_threads"], 3),
+                "fits_per_s_1thread": round(ref["fits"] / ref["seconds_1thread"], 3),
+                "fits_per_s_threads": round(ref["fits"] / ref["seconds_threads"], 3),
+                "gpu_reference_mode_bitwise_equal": f"{same}/{total}"}
+        else:
+            k17["reference_library"] = ref
     return out, k17
+
+
+def reference_library_fits(problems: list[dict]) -> dict:
+    """fit_model of the UNMODIFIED reference library (oracle/_ref/ref_cpu_bench
+    --fits) on the given problems, 1 host thread and all host threads."""
+    import tempfile
+    exe = ROOT / "oracle" / "_ref" / "ref_cpu_bench"
+    if not exe.exists():
+        return {"unavailable": "oracle/_ref/ref_cpu_bench not built (needs /root/reference at build time)"}
+    with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
+        json.dump({"problems": problems}, f)
+        path = f.name
+    try:
+        r = subprocess.run([str(exe), "--fits", path, str(os.cpu_count() or 1)], capture_output=True,
+                           text=True, timeout=1800)
+    finally:
+        os.unlink(path)
+    if r.returncode != 0:
+        return {"error": r.stderr.strip()[-300:]}
+    return json.loads(r.stdout)
 
 
 def model_report(wl, cal, app, mean_s: dict[str, float], dev=None) -> dict:
@@ -738,9 +783,12 @@ def c5_report(dev, parts, variants: list[dict], npts: int = 1_000_000, dist=None
             "gpu_e2e_ms": round(wall * 1e3, 2), "gpu_e2e_evals_per_s": round(nev / wall, 1),
             "cpu_tables_evals_per_s": round(nsub * t.nvar / cpu, 1), "cpu_threads": threads,
             "cpu_max_rel_diff": rel, "argmin_mismatches_vs_cpu": mism,
-            "reference_predict_evals_per_s": round(nref * t.nvar / ref_t, 1),
-            "reference_predict_max_rel_diff": ref_rel,
-            "reference_predict_sample": f"{nref} points x {t.nvar} variants through ps_predict_cpu",
+            # the port's reference-API predict() (features through
+            # evaluate_feature per point): a correctness pin; the reference
+            # LIBRARY's own predict rate is cpu_baseline_reference
+            "port_predict_evals_per_s": round(nref * t.nvar / ref_t, 1),
+            "port_predict_max_rel_diff": ref_rel,
+            "port_predict_sample": f"{nref} points x {t.nvar} variants through ps_predict_cpu",
             "winners": winners}
 
 
@@ -1243,11 +1291,18 @@ def run_ours(args, dist: Dist) -> None:
             "paper_model": ({w: {"all": v["geomean_rel_error_all"],
                                  "ranking_gap_ge_2pct": v["ranking_correct_gap_ge_2pct"]}
                              for w, v in paper.items()} if "error" not in paper else paper)},
-        "model_eval": {k: me.get(k) for k in ("evaluations", "gpu_evals_per_s",
-                                              "gpu_e2e_evals_per_s", "argmin_mismatches_vs_cpu",
-                                              "reference_predict_evals_per_s")} if me else None,
-        "k17": ({k: k17.get(k) for k in ("fits", "launches", "kernel_s", "fits_per_s",
-                                          "cpu_reference_fits", "cpu_reference_fit_s")}
+        "model_eval": dict({k: me.get(k) for k in ("evaluations", "gpu_evals_per_s",
+                                                   "gpu_e2e_evals_per_s", "argmin_mismatches_vs_cpu",
+                                                   "port_predict_max_rel_diff")},
+                           reference_library_predict_evals_per_s=(ref_lib or {}).get(
+                               "predict_evals_per_s"),
+                           reference_library_threads=(ref_lib or {}).get("threads"))
+        if me else None,
+        "k17": ({"fits": k17.get("fits"), "launches": k17.get("launches"),
+                 "kernel_s": k17.get("kernel_s"), "fits_per_s": k17.get("fits_per_s"),
+                 "reference_library": {k: (k17.get("reference_library") or {}).get(k) for k in (
+                     "fits_per_s_1thread", "fits_per_s_threads", "threads",
+                     "gpu_reference_mode_bitwise_equal")}}
                 if k17 and "error" not in k17 else k17),
         "gpu_launches": e2e_launch_total,
         "clocks": {k: clocks.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons")},

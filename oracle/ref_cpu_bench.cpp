@@ -9,14 +9,26 @@
 //                         16Z within [512, 8192], PF/noPF), evals/s on 1 thread
 //                         and on T std::threads (the count cache is shared)
 // usage: ref_cpu_bench [seconds_per_section=2] [threads=hardware]
+//        ref_cpu_bench --fits problems.json [threads=hardware]
+//   the second form runs fit_model on caller-given problems (bench.py: every
+//   model of the round on its measured calibration rows, output-scaled as in
+//   model.cpp:421-435) once on one thread and once spread over T threads,
+//   and prints the fitted parameters (to pin K17's reference mode against the
+//   reference library itself) with both timings.
 // prints one JSON object.
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <string>
 #include <random>
 #include <thread>
 #include <vector>
 
+#include <fstream>
+#include <sstream>
+
+#include "json.hpp"
 #include "perfseer/counting.hpp"
 #include "perfseer/features.hpp"
 #include "perfseer/model.hpp"
@@ -38,7 +50,73 @@ const char* kExpr =
 
 }  // namespace
 
+static int run_fits(const char* path, int threads) {
+  std::ifstream in(path);
+  std::stringstream ss;
+  ss << in.rdbuf();
+  const auto doc = nlohmann::json::parse(ss.str());
+  std::vector<Model> models;
+  std::vector<CalibrationProblem> probs;
+  for (const auto& p : doc.at("problems")) {
+    models.push_back(parse_model_file(p.at("model").get<std::string>()));
+    CalibrationProblem cp;
+    const auto f = p.at("features").get<std::vector<std::vector<double>>>();
+    const auto t = p.at("t").get<std::vector<double>>();
+    for (size_t k = 0; k < t.size(); ++k) cp.rows.push_back(CalibrationRow{f[k], t[k]});
+    probs.push_back(p.value("scale", true) ? scale_features_by_output(cp) : cp);
+  }
+  const size_t n = probs.size();
+  std::vector<std::vector<double>> params(n);
+  std::vector<std::string> errors(n);
+  auto fit_one = [&](size_t i) {
+    try {
+      params[i] = fit_model(models[i], probs[i]).param_vector();
+    } catch (const std::exception& e) {
+      errors[i] = e.what();
+    }
+  };
+  auto t0 = Clock::now();
+  for (size_t i = 0; i < n; ++i) fit_one(i);
+  const double one = secs(t0);
+  t0 = Clock::now();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      for (size_t i = size_t(t); i < n; i += size_t(threads)) fit_one(i);
+    });
+  for (auto& th : pool) th.join();
+  const double many = secs(t0);
+  nlohmann::json out;
+  out["kind"] = "reference";
+  out["library"] = "oracle/_ref/libperfseer_ref.a (unmodified /root/reference/proj/src)";
+  out["fits"] = n;
+  out["seconds_1thread"] = one;
+  out["threads"] = threads;
+  out["seconds_threads"] = many;
+  nlohmann::json ps = nlohmann::json::array();
+  for (size_t i = 0; i < n; ++i) {
+    if (!errors[i].empty()) {
+      ps.push_back(errors[i]);
+      continue;
+    }
+    nlohmann::json v = nlohmann::json::array();
+    for (double x : params[i]) {  // exact bits as hex so nothing is lost in printing
+      uint64_t b;
+      std::memcpy(&b, &x, sizeof b);
+      char buf[24];
+      std::snprintf(buf, sizeof buf, "%016llx", (unsigned long long)b);
+      v.push_back(buf);
+    }
+    ps.push_back(v);
+  }
+  out["params_hex"] = ps;
+  std::printf("%s\n", out.dump().c_str());
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 2 && std::string(argv[1]) == "--fits")
+    return run_fits(argv[2], argc > 3 ? std::atoi(argv[3]) : std::max(1u, std::thread::hardware_concurrency()));
   const double budget = argc > 1 ? std::atof(argv[1]) : 2.0;
   const int threads = argc > 2 ? std::atoi(argv[2]) : std::max(1u, std::thread::hardware_concurrency());
 
