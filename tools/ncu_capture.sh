@@ -37,7 +37,7 @@ cap mm_rm_b matmul_rm "matmul_sq_rm__dtype-float32__groups_fit-True__keep-b__lsi
 cap fd_rm_u finite_diff_strip "finite_diff_rm__dtype-float32__keep-u__n-8176__tile-16x16"
 cap dg_rm_u dg_rm "dg_diff_rm__dtype-float32__keep-u__nelements-1000000__nmatrices-3__nunit_nodes-64__variant-noPF"
 if [ "$only" = "model" ] || [ -z "$only" ]; then
-  for k in lm_batched eval_points; do
+  for k in lm_jobs_kernel eval_points; do
     timeout 600 ncu --set full --clock-control none -k "regex:$k" -c 1 \
       -o $out/ncu_$k -f python tools/run_model_kernels.py > $out/ncu_$k.log 2>&1
     echo "$k rc=$?"
@@ -46,6 +46,6 @@ fi
 if [ -z "$only" ] || [ "$only" = "launches" ]; then
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 8000 --csv \
   --log-file $out/launches_all.csv python bench.py --steps 1 --warmup 3 --trials-per-step 1 \
-  --c5-points 100000 --tc 0 > $out/launches_bench.log 2>&1
+  --c5-points 100000 --tc 0 --detail $out/launches_detail.json > $out/launches_bench.log 2>&1
 echo "launches rc=$?"
 fi
