@@ -1,0 +1,67 @@
+"""Held-out model selection (bench.headline / bench._errors): the headline
+model is chosen on the workload's validation sizes only and scored on the
+rest; the paper's per-variant linear/nonlinear choice follows the majority of
+the work-removal diagnosis."""
+from __future__ import annotations
+
+import numpy as np
+
+
+def _app():
+    from paper_1904_09538_b200 import workloads
+    wl = workloads.MATMUL
+    ids = [f"matmul_sq__dtype-float32__groups_fit-True__lsize_0-16__lsize_1-16__n-{n}"
+           f"__prefetch-{pf}" for n in (512, 1024, 2048, 4096) for pf in ("True", "False")]
+    return wl, ids
+
+
+def test_errors_split_validation_and_test():
+    import bench
+    wl, app = _app()
+    meas = np.ones(len(app))
+    pred = np.array([1.1 if "n-1024" in k or "n-4096" in k else 1.3 for k in app])
+    e = bench._errors(wl, app, pred, meas)
+    assert abs(e["validation_geomean_rel_error"] - 0.1) < 1e-12
+    assert abs(e["test"]["geomean_rel_error_all"] - 0.3) < 1e-12
+    assert e["test"]["rows"] == 4
+
+
+def test_headline_uses_validation_error_only():
+    import bench
+    models = {
+        # better on test, worse on validation: must NOT win
+        "a": {"gpu_reference_fit": {"calibration_geomean_rel_error": 0.01,
+                                    "validation_geomean_rel_error": 0.20,
+                                    "test": {"geomean_rel_error_all": 0.01}}},
+        "b": {"gpu_multistart_fit": {"calibration_geomean_rel_error": 0.05,
+                                     "validation_geomean_rel_error": 0.10,
+                                     "test": {"geomean_rel_error_all": 0.40}}},
+        "c": {"gpu_multistart_fit": {"error": "diverged"}},
+    }
+    m, fit, rec = bench.headline(models)
+    assert (m, fit) == ("b", "gpu_multistart_fit")
+    # forcing a model falls back to its lowest calibration error
+    m, fit, _ = bench.headline(models, "a")
+    assert (m, fit) == ("a", "gpu_reference_fit")
+
+
+def test_paper_selection_follows_majority_diagnosis():
+    import bench
+    from paper_1904_09538_b200 import host, workloads
+    wl, app = _app()
+    mean_s = {k: 1e-3 for k in app}
+    fits = {}
+    for name in ("linear", "nonlinear"):
+        m = host.HostModel(wl.models[name])
+        fits[name] = {"gpu_reference_fit": {"calibration_geomean_rel_error": 0.1,
+                                            "params": {p: 1e-12 for p in m.params}}}
+    diag = {"matmul": {"matmul_sq_prefetch-True": {"n=512": {"kind": "linear"},
+                                                   "n=1024": {"kind": "linear"},
+                                                   "n=2048": {"kind": "max_overlap"}},
+                       "matmul_sq_prefetch-False": {"n=512": {"kind": "max_overlap"},
+                                                    "n=1024": {"kind": "max_overlap"}}}}
+    out = bench.paper_selection([(wl, [], app)], {"matmul": fits}, diag, mean_s)
+    assert out["matmul"]["choice"] == {"matmul_sq_prefetch-True": "linear",
+                                       "matmul_sq_prefetch-False": "nonlinear"}
+    assert set(out["matmul"]["geomean_rel_error"]) == {"matmul_sq_prefetch-True",
+                                                       "matmul_sq_prefetch-False"}
