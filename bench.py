@@ -990,6 +990,9 @@ def run_ours(args, dist: Dist) -> None:
     cross_rank = {"kernel": ref_vid, "seconds_per_rank": [round(float(x), 9) for x in per_rank],
                   "max_over_min": round(float(per_rank.max() / per_rank.min()), 4)}
 
+    # the sweep's resident arrays are no longer needed: the e2e pass places
+    # every kernel's arrays in one device arena instead
+    dev.trim()
     # e2e through host buffers (ps_run_host: H2D + kernel + D2H per launch)
     e2e_set = [i for i in my_kernels if e2e_owner.get(i) == dist.rank
                and not (descs[i].gen in (1, 6) and descs[i].nelements > (1 << 28))]
@@ -1073,8 +1076,8 @@ def run_ours(args, dist: Dist) -> None:
     for ins, outs in pinned.values():
         for a in ins + outs:
             a.free()
-    # the sweep's resident arrays are no longer needed: give the fits, the
-    # prediction tables and the variant reports their HBM back
+    # give the fits, the prediction tables and the variant reports the HBM
+    # the e2e arena held
     dev.trim()
 
     # ----- measurement table -> summaries (every rank holds the gathered table) -----

@@ -838,7 +838,7 @@ int ps_destroy(ps_ctx* ctx) {
   cudaStreamSynchronize(c->stream);
   for (auto& kv : c->slots) c->release(kv.second);
   c->release(c->host_slot);
-  for (auto& ps : c->pipe_slot) c->release(ps);
+  if (c->arena.ptr) cudaFree(c->arena.ptr);
   for (auto& row : c->pipe_ev)
     for (auto e : row)
       if (e) cudaEventDestroy(e);
@@ -1088,55 +1088,105 @@ int ps_run_host_batch_ex(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const 
   *seconds = 0.0;
   if (n == 0) return PS_OK;
   PS_CUDA(cudaSetDevice(c->device));
+  // Every kernel's arrays get a region of one device arena, placed as a ring
+  // in batch order. The copy-in stream only waits where a region is reused
+  // (for the launch — and the copy-out — of the kernel that last held those
+  // bytes), so the H2D engine runs ahead by BYTES, across any number of
+  // short kernels, while long kernels compute; when the whole batch fits (the
+  // bench's sweep: ~115 GB) nothing is ever reused and the copy engines and
+  // the SMs overlap for the whole pass.
+  auto al = [](size_t b) { return (b + 511) & ~size_t(511); };
   std::vector<ps_io_info> io(n);
-  constexpr int NS = Ctx::kPipeSlots;
-  size_t need[NS][2][PS_MAX_ARRAYS] = {};  // [slot][in/out][array] bytes
+  std::vector<size_t> need(n);
+  size_t total = 0, biggest = 0;
   int rc;
   for (int i = 0; i < n; ++i) {
     if ((rc = validate_desc(&descs[i])) || (rc = kernel_io(&descs[i], &io[i]))) return rc;
-    for (int a = 0; a < io[i].n_inputs; ++a)
-      need[i % NS][0][a] = std::max(need[i % NS][0][a], (size_t)io[i].input_elems[a] * io[i].elem_bytes);
-    for (int a = 0; a < io[i].n_outputs; ++a)
-      need[i % NS][1][a] = std::max(need[i % NS][1][a], (size_t)io[i].output_elems[a] * io[i].elem_bytes);
+    size_t b = 0;
+    for (int a = 0; a < io[i].n_inputs; ++a) b += al((size_t)io[i].input_elems[a] * io[i].elem_bytes);
+    for (int a = 0; a < io[i].n_outputs; ++a) b += al((size_t)io[i].output_elems[a] * io[i].elem_bytes);
+    need[i] = std::max<size_t>(b, 512);
+    total += need[i];
+    biggest = std::max(biggest, need[i]);
   }
-  // every allocation before the timed region (cudaMalloc synchronises)
-  for (int sl = 0; sl < NS; ++sl)
-    for (int a = 0; a < PS_MAX_ARRAYS; ++a) {
-      if (need[sl][0][a] && (rc = c->ensure(c->pipe_slot[sl].in[a], need[sl][0][a]))) return rc;
-      if (need[sl][1][a] && (rc = c->ensure(c->pipe_slot[sl].out[a], need[sl][1][a]))) return rc;
+  // arena: the whole batch if HBM allows (resident sweep variants are evicted
+  // by Ctx::ensure when needed), else as much as fits above the largest kernel
+  size_t fr = 0, tot = 0;
+  PS_CUDA(cudaMemGetInfo(&fr, &tot));
+  const size_t budget = tot > (size_t)12e9 ? tot - (size_t)10e9 : tot / 2;
+  size_t want = std::max(biggest, std::min(total, budget));
+  if (const char* mb = getenv("PS_E2E_ARENA_MB"))  // tests: force ring reuse
+    want = std::max(biggest, std::min(want, (size_t)(atof(mb) * 1048576.0)));
+  if (c->arena.cap < want || c->arena.cap > want + want / 2) {
+    if (c->arena.ptr) cudaFree(c->arena.ptr);
+    c->arena = DevBuf{};
+    if ((rc = c->ensure(c->arena, want))) {
+      // fall back to the largest kernel's footprint (no lookahead beyond it)
+      cudaGetLastError();
+      if ((rc = c->ensure(c->arena, biggest))) return rc;
     }
+  }
+  const size_t cap = c->arena.cap;
+  char* base = static_cast<char*>(c->arena.ptr);
   if (!c->h2d_stream) PS_CUDA(cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking));
   if (!c->d2h_stream) PS_CUDA(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
   for (auto& row : c->pipe_ev)
-    for (auto& e : row)
-      if (!e) PS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    while ((int)row.size() < n) {
+      cudaEvent_t e;
+      PS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      row.push_back(e);
+    }
+  std::vector<cudaEvent_t>& h2d_done = c->pipe_ev[0];
+  std::vector<cudaEvent_t>& run_done = c->pipe_ev[1];
+  std::vector<cudaEvent_t>& d2h_done = c->pipe_ev[2];
   if ((rc = events(c, 2))) return rc;
   unsigned long long* dsum = nullptr;
   if (checksums) {
     if ((rc = c->ensure(c->scratch[6], sizeof(unsigned long long) * (size_t)n))) return rc;
     dsum = reinterpret_cast<unsigned long long*>(c->scratch[6].ptr);
   }
-  cudaEvent_t(&h2d_done)[NS] = c->pipe_ev[0];
-  cudaEvent_t(&run_done)[NS] = c->pipe_ev[1];
-  cudaEvent_t(&d2h_done)[NS] = c->pipe_ev[2];
   c->prepared = false;
   PS_CUDA(cudaEventRecord(c->ev[0], c->stream));
   PS_CUDA(cudaStreamWaitEvent(c->h2d_stream, c->ev[0], 0));
   PS_CUDA(cudaStreamWaitEvent(c->d2h_stream, c->ev[0], 0));
   if (dsum) PS_CUDA(cudaMemsetAsync(dsum, 0, sizeof(unsigned long long) * (size_t)n, c->stream));
-  size_t in_at = 0, out_at = 0;
+  struct Live {
+    int k;
+    size_t lo, hi;
+  };
+  std::vector<Live> live;  // regions still in use, oldest first
+  size_t pos = 0, in_at = 0, out_at = 0;
   for (int i = 0; i < n; ++i) {
-    const int sl = i % NS;
-    Slot& s = c->pipe_slot[sl];
-    // copy in once the launch two kernels back has consumed this slot's inputs
-    if (i >= NS) PS_CUDA(cudaStreamWaitEvent(c->h2d_stream, run_done[sl], 0));
+    if (pos + need[i] > cap) pos = 0;  // wrap
+    const size_t lo = pos, hi = pos + need[i];
+    pos = hi;
+    // wait for every earlier kernel whose bytes this region reuses
+    for (size_t q = 0; q < live.size();) {
+      const Live& L = live[q];
+      if (L.lo < hi && lo < L.hi) {
+        PS_CUDA(cudaStreamWaitEvent(c->h2d_stream, run_done[L.k], 0));
+        if (outputs) PS_CUDA(cudaStreamWaitEvent(c->h2d_stream, d2h_done[L.k], 0));
+        live.erase(live.begin() + (long)q);
+      } else {
+        ++q;
+      }
+    }
+    live.push_back(Live{i, lo, hi});
+    Slot s;
+    size_t at = lo;
+    for (int a = 0; a < io[i].n_inputs; ++a) {
+      s.in[a].ptr = base + at;
+      at += al((size_t)io[i].input_elems[a] * io[i].elem_bytes);
+    }
+    for (int a = 0; a < io[i].n_outputs; ++a) {
+      s.out[a].ptr = base + at;
+      at += al((size_t)io[i].output_elems[a] * io[i].elem_bytes);
+    }
     for (int a = 0; a < io[i].n_inputs; ++a)
       PS_CUDA(cudaMemcpyAsync(s.in[a].ptr, inputs[in_at + a], (size_t)io[i].input_elems[a] * io[i].elem_bytes,
                               cudaMemcpyHostToDevice, c->h2d_stream));
-    PS_CUDA(cudaEventRecord(h2d_done[sl], c->h2d_stream));
-    // launch once the inputs are in and the slot's previous outputs are out
-    PS_CUDA(cudaStreamWaitEvent(c->stream, h2d_done[sl], 0));
-    if (i >= NS && outputs) PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[sl], 0));
+    PS_CUDA(cudaEventRecord(h2d_done[i], c->h2d_stream));
+    PS_CUDA(cudaStreamWaitEvent(c->stream, h2d_done[i], 0));
     s.io = io[i];
     c->activate(s);
     if ((rc = launch(c, &descs[i]))) return rc;
@@ -1146,21 +1196,19 @@ int ps_run_host_batch_ex(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const 
         const int blocks = (int)std::min<int64_t>((words + 255) / 256, (int64_t)c->sm_count * 8);
         word_checksum<<<std::max(blocks, 1), 256, 0, c->stream>>>((const uint32_t*)s.out[a].ptr, words, dsum + i);
       }
-    PS_CUDA(cudaEventRecord(run_done[sl], c->stream));
+    PS_CUDA(cudaEventRecord(run_done[i], c->stream));
     if (outputs) {
-      PS_CUDA(cudaStreamWaitEvent(c->d2h_stream, run_done[sl], 0));
+      PS_CUDA(cudaStreamWaitEvent(c->d2h_stream, run_done[i], 0));
       for (int a = 0; a < io[i].n_outputs; ++a)
         PS_CUDA(cudaMemcpyAsync(outputs[out_at + a], s.out[a].ptr,
                                 (size_t)io[i].output_elems[a] * io[i].elem_bytes, cudaMemcpyDeviceToHost,
                                 c->d2h_stream));
-      PS_CUDA(cudaEventRecord(d2h_done[sl], c->d2h_stream));
+      PS_CUDA(cudaEventRecord(d2h_done[i], c->d2h_stream));
     }
     in_at += io[i].n_inputs;
     out_at += io[i].n_outputs;
   }
-  if (outputs) {
-    for (int k = std::max(0, n - NS); k < n; ++k) PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[k % NS], 0));
-  }
+  if (outputs) PS_CUDA(cudaStreamWaitEvent(c->stream, d2h_done[n - 1], 0));  // d2h stream is in order
   if (dsum)  // the step's result: one checksum per kernel
     PS_CUDA(cudaMemcpyAsync(checksums, dsum, sizeof(unsigned long long) * (size_t)n, cudaMemcpyDeviceToHost,
                             c->stream));
@@ -1169,6 +1217,7 @@ int ps_run_host_batch_ex(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const 
   float ms = 0.f;
   PS_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
   *seconds = (double)ms * 1e-3;
+  c->activate(c->host_slot);  // no dangling views into the arena
   return PS_OK;
 }
 
@@ -1181,7 +1230,8 @@ int ps_trim(ps_ctx* ctx) {
   c->slots.clear();
   c->cache_bytes = 0;
   c->release(c->host_slot);
-  for (auto& ps : c->pipe_slot) c->release(ps);
+  if (c->arena.ptr) cudaFree(c->arena.ptr);
+  c->arena = DevBuf{};
   c->prepared = false;
   return PS_OK;
 }

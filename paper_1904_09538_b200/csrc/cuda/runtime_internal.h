@@ -44,12 +44,12 @@ struct Ctx {
   DevBuf scratch[8];
   std::map<std::string, Slot> slots;  // keyed by the raw descriptor bytes
   Slot host_slot;                     // caller-data runs (verify / run_host)
-  // ps_run_host_batch: kPipeSlots device slots, copy-in / copy-out streams and the
-  // per-slot events that order them against the launches on `stream`
-  static constexpr int kPipeSlots = 4;
-  Slot pipe_slot[kPipeSlots];
+  // ps_run_host_batch: one device arena the kernels' arrays are placed in as
+  // a ring (byte-level lookahead for the copy engines), copy-in / copy-out
+  // streams and per-kernel events ordering them against the launches
+  DevBuf arena;
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
-  cudaEvent_t pipe_ev[3][kPipeSlots] = {};  // [h2d done, launch done, d2h done][slot]
+  std::vector<cudaEvent_t> pipe_ev[3];  // [h2d done, launch done, d2h done][kernel]
   size_t cache_bytes = 0, cache_cap = 0;
   uint64_t tick = 0;
   bool prepared = false;

@@ -68,3 +68,34 @@ def test_batch_checksums_equal_host_sums_of_outputs():
         for arrs in ins_all:
             for a in arrs:
                 a.free()
+
+
+def test_batch_with_a_small_arena_reuses_regions_correctly(monkeypatch):
+    """A device arena smaller than the batch: regions are reused as a ring and
+    the copy-in of a kernel waits for the launch (and copy-out) of the kernel
+    that last held its bytes — outputs still equal the single-launch hook."""
+    from paper_1904_09538_b200.device import CudaDevice, PinnedArray
+    ids = IDS * 3  # 15 kernels through an arena of ~2 of them
+    monkeypatch.setenv("PS_E2E_ARENA_MB", "20")
+    with CudaDevice(0) as dev:
+        ins_all, outs_all, want = [], [], []
+        for vid in ids:
+            d, io = desc_io(vid)
+            ins = make_inputs(d, io, "uniform", seed=len(ins_all))
+            want.append(dev.run(d, ins))
+            pins = []
+            for a in ins:
+                p = PinnedArray(a.nbytes)
+                p.numpy(a.dtype)[:] = a
+                pins.append(p)
+            ins_all.append(pins)
+            outs_all.append([PinnedArray(int(io.output_elems[j]) * io.elem_bytes)
+                             for j in range(io.n_outputs)])
+        for _ in range(2):
+            assert dev.run_host_batch(ids, ins_all, outs_all) > 0
+            for vid, outs, w in zip(ids, outs_all, want):
+                for o, ref in zip(outs, w):
+                    assert np.array_equal(o.numpy(ref.dtype).view(np.uint8), ref.view(np.uint8)), vid
+        for arrs in ins_all + outs_all:
+            for a in arrs:
+                a.free()
