@@ -193,7 +193,9 @@ __global__ void __launch_bounds__(kLmThreads) lm_batched_kernel(LmArgs A) {
   __shared__ double p[kLmMaxParams], cand[kLmMaxParams], scale[kLmMaxParams];
   __shared__ double jtj[kLmMaxParams * kLmMaxParams], jtr[kLmMaxParams];
   __shared__ double red;
-  __shared__ int flag_sh;  // 0 continue, 1 converged, 2 diverged, 3 singular
+  __shared__ int flag_sh;   // gradient / step test: 1 converged
+  __shared__ int solve_sh;  // damped solve: 0 ok, 2 diverged, 3 singular (own word: thread 0
+                            // writes it while other threads may still read flag_sh)
 
   if (threadIdx.x < np) {
     const double p0 = A.params[(size_t)b * np + threadIdx.x];
@@ -257,9 +259,9 @@ __global__ void __launch_bounds__(kLmThreads) lm_batched_kernel(LmArgs A) {
     bool accepted = false;
     while (!accepted) {
       if (threadIdx.x == 0) {
-        flag_sh = 0;
+        solve_sh = 0;
         if (lambda > 1e100) {
-          flag_sh = 2;
+          solve_sh = 2;
         } else {
           double a[kLmMaxParams][kLmMaxParams + 1];
           for (int i = 0; i < np; ++i) {
@@ -267,12 +269,12 @@ __global__ void __launch_bounds__(kLmThreads) lm_batched_kernel(LmArgs A) {
             a[i][i] += lambda;
             a[i][np] = jtr[i];
           }
-          for (int col = 0; col < np && flag_sh == 0; ++col) {
+          for (int col = 0; col < np && solve_sh == 0; ++col) {
             int piv = col;
             for (int r = col + 1; r < np; ++r)
               if (fabs(a[r][col]) > fabs(a[piv][col])) piv = r;
             if (fabs(a[piv][col]) < 1e-300) {
-              flag_sh = 3;
+              solve_sh = 3;
               break;
             }
             if (piv != col)
@@ -288,7 +290,7 @@ __global__ void __launch_bounds__(kLmThreads) lm_batched_kernel(LmArgs A) {
               a[r][np] -= fct * a[col][np];
             }
           }
-          if (flag_sh == 0) {
+          if (solve_sh == 0) {
             double x[kLmMaxParams];
             for (int col = np - 1; col >= 0; --col) {
               double acc = a[col][np];
@@ -304,11 +306,11 @@ __global__ void __launch_bounds__(kLmThreads) lm_batched_kernel(LmArgs A) {
         }
       }
       __syncthreads();
-      if (flag_sh == 2) {
+      if (solve_sh == 2) {
         status = 1;
         break;
       }
-      if (flag_sh == 3) {
+      if (solve_sh == 3) {
         lambda *= A.opt.lambda_increase;
         __syncthreads();
         continue;

@@ -211,7 +211,9 @@ __global__ void __launch_bounds__(kJobThreads) lm_jobs_kernel(const DevJob* __re
   __shared__ double jtj[kJobMaxParams * kJobMaxParams], jtr[kJobMaxParams];
   __shared__ double aug[kJobMaxParams * (kJobMaxParams + 1)];
   __shared__ double red;
-  __shared__ int flag_sh;  // 0 continue, 1 converged, 2 diverged, 3 singular
+  __shared__ int flag_sh;   // gradient / step test: 1 converged
+  __shared__ int solve_sh;  // damped solve: 0 ok, 2 diverged, 3 singular (its own word: warp 0
+                            // writes it while other warps may still read flag_sh)
 
   Fit F;
   F.J = &J;
@@ -296,14 +298,14 @@ __global__ void __launch_bounds__(kJobThreads) lm_jobs_kernel(const DevJob* __re
             cand[lane] = v;
           }
         }
-        if (lane == 0) flag_sh = fl;
+        if (lane == 0) solve_sh = fl;
       }
       __syncthreads();
-      if (flag_sh == 2) {
+      if (solve_sh == 2) {
         status = 1;
         break;
       }
-      if (flag_sh == 3) {
+      if (solve_sh == 3) {
         lambda *= opt.lambda_increase;
         __syncthreads();
         continue;
