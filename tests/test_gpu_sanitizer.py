@@ -20,7 +20,7 @@ K17_K18 = r'''
 import sys; sys.path.insert(0, ".")
 import numpy as np
 from paper_1904_09538_b200 import host, workloads
-from paper_1904_09538_b200.device import CudaDevice, fit_lm_jobs
+from paper_1904_09538_b200.device import CudaDevice, fit_lm_batched, fit_lm_jobs
 from paper_1904_09538_b200.predict import PredictionTables, c5_points
 rng = np.random.default_rng(1)
 with CudaDevice(0) as dev:
@@ -35,6 +35,9 @@ with CudaDevice(0) as dev:
         jobs.append({"model": m, "features": F / t[:, None], "t": np.ones_like(t), "mode": 0,
                      "starts": m.initial_point(F / t[:, None], np.ones_like(t), scale=0)[None]})
     res, _ = fit_lm_jobs(dev, jobs)
+    # the round-1 K17 (postfix bytecode, forward-mode derivatives) as well
+    j = jobs[0]
+    fit_lm_batched(dev, j["model"], j["features"], j["t"], j["starts"], mode=13)
     vid = "matmul_sq__dtype-float32__groups_fit-True__lsize_0-16__lsize_1-16__n-1024__prefetch-True"
     m = host.HostModel(workloads.MATMUL.models["ldst"])
     t = PredictionTables([{"id": vid, "model": m.text, "params": list(res[0][0][0]), "group": 0,
