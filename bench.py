@@ -994,8 +994,9 @@ def run_ours(args, dist: Dist) -> None:
     # every kernel's arrays in one device arena instead
     dev.trim()
     # e2e through host buffers (ps_run_host: H2D + kernel + D2H per launch)
-    e2e_set = [i for i in my_kernels if e2e_owner.get(i) == dist.rank
-               and not (descs[i].gen in (1, 6) and descs[i].nelements > (1 << 28))]
+    # every kernel of the sweep (the same workload as `value`), each on the
+    # rank holding its first trial
+    e2e_set = [i for i in my_kernels if e2e_owner.get(i) == dist.rank]
     # pinned host memory: ranks on one host share its RAM; the output arrays
     # (only the e2e_full_outputs pass needs them) are dropped first if the
     # rank's share would be exceeded
