@@ -226,7 +226,7 @@ def estimate_seconds(io) -> float:
     return io.bytes_global / 6.0e12 + io.flops / 30e12 + io.bytes_shared / 30e12 + 4e-6
 
 
-def previous_run_seconds(path: Path = ROOT / "profiles" / "r01_table_all.csv") -> dict[str, float]:
+def previous_run_seconds(path: Path = ROOT / "profiles" / "r02_table_all.csv") -> dict[str, float]:
     """Per-kernel mean seconds of the last committed sweep (LPT
     on the previous run's times); kernels it lacks fall back to
     estimate_seconds. On the round-1 table the crude estimate balances 8
@@ -1031,14 +1031,21 @@ def run_ours(args, dist: Dist) -> None:
     # e2e: the step's result read back is one device checksum per kernel (the
     # sweep's product is its timing table, the output arrays are scratch);
     # e2e_full_outputs: every output array copied back as well.
-    # order the batch so copy-heavy and launch-heavy kernels alternate: the
-    # copy-in engine then works ahead during long launches instead of the
-    # pipeline stalling on back-to-back large copies (the product is per
-    # kernel, so the order within a step is free)
-    def h2d_minus_run(i: int) -> float:
-        return (sum(a.nbytes for a in pinned[i][0]) / 50e9) - (prev.get(kernels[i]) or est[i])
-    by = sorted(e2e_set, key=h2d_minus_run, reverse=True)
-    e2e_set = [by[j // 2] if j % 2 == 0 else by[len(by) - 1 - j // 2] for j in range(len(by))]
+    # Order the batch by Johnson's rule for the two-stage flow shop copy-in ->
+    # launch (the device arena gives the copy engine unlimited lookahead, so
+    # this order minimises the pass's makespan): kernels whose copy is shorter
+    # than their run first, by increasing copy time (the SMs start at once
+    # and the copy engine gets ahead), then the copy-dominated ones by
+    # decreasing run time. The product is per kernel, so the order within a
+    # step is free.
+    def copy_s(i: int) -> float:
+        return sum(a.nbytes for a in pinned[i][0]) / 50e9
+
+    def run_s(i: int) -> float:
+        return prev.get(kernels[i]) or est[i]
+    first = sorted((i for i in e2e_set if copy_s(i) < run_s(i)), key=copy_s)
+    last = sorted((i for i in e2e_set if copy_s(i) >= run_s(i)), key=run_s, reverse=True)
+    e2e_set = first + last
     batch = [descs[i] for i in e2e_set]
     b_in = [pinned[i][0] for i in e2e_set]
     b_out = [pinned[i][1] for i in e2e_set]
