@@ -227,6 +227,7 @@ int ps_fit_lm_jobs(ps_ctx* ctx, int njobs, const ps_lm_job* jobs, double* kernel
     if (!ctx || !jobs || njobs < 1) throw EvalError("ps_fit_lm_jobs: bad argument");
     // one value program and one value+Jacobian program per distinct model text
     std::map<std::string, std::pair<Program, Program>> progs;
+    std::map<std::string, int> nfeat;
     std::vector<ps::LmJobHost> hj(static_cast<size_t>(njobs));
     for (int j = 0; j < njobs; ++j) {
       const ps_lm_job& in = jobs[j];
@@ -235,12 +236,15 @@ int ps_fit_lm_jobs(ps_ctx* ctx, int njobs, const ps_lm_job* jobs, double* kernel
       auto it = progs.find(in.model_text);
       if (it == progs.end()) {
         Model m = model_from_text(in.model_text);
-        if (int(m.features.size()) != in.nf)
-          throw EvalError("ps_fit_lm_jobs: job " + std::to_string(j) + ": model has " +
-                          std::to_string(m.features.size()) + " features, job gives " + std::to_string(in.nf));
+        nfeat[in.model_text] = int(m.features.size());
         it = progs.emplace(in.model_text, std::make_pair(compile_model_program(m, false),
                                                          compile_model_program(m, true))).first;
       }
+      if (nfeat[in.model_text] != in.nf)
+        throw EvalError("ps_fit_lm_jobs: job " + std::to_string(j) + ": model has " +
+                        std::to_string(nfeat[in.model_text]) + " features, job gives " + std::to_string(in.nf));
+      if (in.nr < 1 || in.nbatch < 1)
+        throw EvalError("ps_fit_lm_jobs: job " + std::to_string(j) + ": nr and nbatch must be >= 1");
       auto view = [](const Program& pr) {
         return ps::LmProgramHost{pr.insns.data(), pr.consts.data(), pr.outputs.data(), int(pr.insns.size() / 2),
                                  int(pr.consts.size()), int(pr.outputs.size()), pr.n_slots};

@@ -217,3 +217,17 @@ def test_lm_jobs_multistart_shuffle_matches_single_starts(dev):
     res, _ = fit_lm_jobs(dev, [{"model": m, "features": F, "t": t, "starts": starts, "mode": 7},
                                {"model": m, "features": F, "t": t, "starts": starts[1:2], "mode": 7}])
     np.testing.assert_array_equal(res[0][0][1], res[1][0][0])
+
+
+def test_lm_jobs_rejects_bad_jobs(dev):
+    from paper_1904_09538_b200 import PsError, host, workloads
+    from paper_1904_09538_b200.device import fit_lm_jobs
+    m = host.HostModel(workloads.MATMUL.models["linear"])
+    F = np.ones((20, len(m.features)))
+    good = {"model": m, "features": F, "t": np.ones(20), "starts": np.ones((1, len(m.params)))}
+    # second job with the same model text but the wrong feature count
+    bad = dict(good, features=np.ones((20, len(m.features) - 1)))
+    with pytest.raises(PsError, match="features"):
+        fit_lm_jobs(dev, [good, bad])
+    with pytest.raises(PsError, match="rank deficiency"):
+        fit_lm_jobs(dev, [dict(good, features=F[:3], t=np.ones(3))])
