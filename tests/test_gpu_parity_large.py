@@ -149,3 +149,31 @@ def test_tc_8192_sampled_rows(dev):
     exact = a[rows] @ b
     bound = 2.0 ** -10 * (np.abs(a[rows]) @ np.abs(b))
     assert np.all(np.abs(got[rows] - exact) <= bound)
+
+
+@pytest.mark.parametrize("np_", [16, 32, 48, 64, 96, 128])
+@pytest.mark.parametrize("variant", ["noPF", "uPF", "dmPF", "dmPFtrans", "tc"])
+def test_dg_1e6_sampled_elements(dev, variant, np_):
+    """The bench's largest DG size (nel = 10^6) for every variant, K19
+    included: seed-pattern inputs are small integers, so every partial sum is
+    exact and res[m, k, i] = sum_j dm[m, i, j] u[k, j] in float64 at sampled
+    elements k is the bitwise answer regardless of summation order."""
+    nel, nmat = 1_000_000, 3
+    if variant == "tc":
+        v = f"dg_diff_tc__dtype-float32__nelements-{nel}__nmatrices-{nmat}__nunit_nodes-{np_}"
+    else:
+        v = vid("dg_diff", dtype="float32", variant=variant, nelements=nel, nunit_nodes=np_,
+                nmatrices=nmat)
+    d, io = desc_io(v)
+    ins = make_inputs(d, io, "seed17")
+    got = dev.run(d, ins)[0]
+    dm = ins[0].astype(np.float64).reshape(nmat, np_, np_)
+    trans = variant == "dmPFtrans"
+    u = ins[1].astype(np.float64)
+    u = u.reshape(np_, nel).T if trans else u.reshape(nel, np_)
+    rng = np.random.default_rng(np_)
+    ks = np.concatenate([rng.choice(nel, 500, replace=False), [0, 127, 128, nel - 1]])
+    want = np.einsum("mij,kj->mki", dm, u[ks])  # [m, k, i]
+    g = got.reshape(nmat, np_, nel)[:, :, ks].transpose(0, 2, 1) if trans else \
+        got.reshape(nmat, nel, np_)[:, ks, :]
+    np.testing.assert_array_equal(g.astype(np.float64), want)
