@@ -10,6 +10,7 @@ sizes bench.py times, not only the small parity cases.
 * finite_diff and finite_diff_rm, both tiles, at n = 8176 (full oracle);
 * DG, all four variants at nel = 10^5 and every padded Np of orders 1-7
   (16, 32, 48, 64, 96, 128), and their work-removed kernels at Np = 32;
+  at the bench's nel = 10^6 every variant and K19 on sampled elements;
 * gmem_pattern k = 1, 2 at E = 2^28 (1 GiB per array);
 * the tcgen05 variant K16 at n = 8192 on sampled rows: bitwise on
   seed-pattern inputs, within the TF32 bound (fp64 reference rows) on U[-1,1).
