@@ -238,7 +238,7 @@ FD = Workload(
             "ldst": ldst_model(FD_LOADS, FD_STORES, ONCHIP[:3], ONCHIP[3:]),
             "ldst_g": ldst_model(FD_LOADS, FD_STORES, ONCHIP[:3], ONCHIP[3:], group_pipe=True)},
     variant_keys=("tile",),
-    validation_sizes=("n=1120", "n=4480"),
+    validation_sizes=("n=1120", "n=2240"),
     size_keys=("n",),
     extra={"options": {"partial_subgroups": "round_up"}},
     c5_coords={"n": 1},

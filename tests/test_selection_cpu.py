@@ -65,3 +65,25 @@ def test_paper_selection_follows_majority_diagnosis():
                                        "matmul_sq_prefetch-False": "nonlinear"}
     assert set(out["matmul"]["geomean_rel_error"]) == {"matmul_sq_prefetch-True",
                                                        "matmul_sq_prefetch-False"}
+
+
+def test_per_variant_selection_ranks_first_then_error_on_validation_only():
+    import bench
+    wl, app = _app()  # matmul PF/noPF at n = 512, 1024, 2048, 4096; validation 1024, 4096
+    meas = {k: (1.0 if "prefetch-True" in k else 1.2) for k in app}
+    # candidate A: PF accurate everywhere, noPF 30% low on validation -> ranks wrong
+    # candidate B: PF 8% high, noPF 5% high on validation (ranks right), awful on test
+    pa = {k: meas[k] * (1.0 if "prefetch-True" in k else 0.7) for k in app}
+    pb = {k: meas[k] * ((1.08 if "prefetch-True" in k else 1.05)
+                        if ("n-1024" in k or "n-4096" in k) else 3.0) for k in app}
+    bench.APP_PREDICTIONS.clear()
+    bench.APP_PREDICTIONS[("matmul", "a", "gpu_reference_fit")] = pa
+    bench.APP_PREDICTIONS[("matmul", "b", "gpu_multistart_fit")] = pb
+    r = bench.select_per_variant(wl, app, meas)
+    bench.APP_PREDICTIONS.clear()
+    # PF: A (exact); noPF: B — the only way to rank n=1024/4096 right; the
+    # test sizes (where B is off by 3x) never enter the choice
+    assert r["assignment"] == {"matmul_sq_prefetch-True": "a/gpu_reference_fit",
+                               "matmul_sq_prefetch-False": "b/gpu_multistart_fit"}
+    assert r["validation_ranking_correct_gap_ge_2pct"] == "2/2"
+    assert r["test"]["geomean_rel_error"]["matmul_sq_prefetch-False"] > 1.0
