@@ -344,7 +344,10 @@ int ps_model_program(const char* model_text, int with_jacobian, char* out, size_
  * when a work-group is not a whole number of sub-groups) | round_up
  * (ceil(wg/32) sub-groups); "launch_geometry" = realised
  * (vectorised row sweeps, FD strips) | literal (one CTA per IR work-group,
- * the grid/block of launch_geometry, transforms.cpp:242-275). */
+ * the grid/block of launch_geometry, transforms.cpp:242-275);
+ * "measure_queue_ahead" = on (default: ps_measure enqueues a short idle
+ * kernel before the timed trials so each event pair brackets device work
+ * only, like the OpenCL profiling timestamps the paper reads) | off. */
 int ps_set_option(const char* key, const char* value);
 /* geo_mean_rel_error (executor.cpp:50-61). */
 int ps_geo_mean_rel_error(const double* pred, const double* meas, int n, double* out);

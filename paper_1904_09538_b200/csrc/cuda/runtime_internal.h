@@ -124,6 +124,8 @@ int bytecode_depth(const int32_t* ops, int n_ops, int n_consts, int np, int nf);
 // Launch geometry switch (runtime.cu): literal = one CTA per IR work-group.
 void set_literal_geometry(bool on);
 bool literal_geometry();
+// Queue-ahead kernel before ps_measure's timed trials (on by default).
+void set_queue_ahead(bool on);
 
 // K17 v2 (lm_jobs.cu): straight-line model programs (host-compiled,
 // perfseer::compile_program) and one fit job per (model, problem, starts).

@@ -284,6 +284,11 @@ int ps_set_option(const char* key, const char* value) {
       ps::set_literal_geometry(v == "literal");
       return PS_OK;
     }
+    if (k == "measure_queue_ahead") {
+      if (v != "on" && v != "off") throw EvalError("measure_queue_ahead: on | off");
+      ps::set_queue_ahead(v == "on");
+      return PS_OK;
+    }
     throw EvalError("unknown option '" + k + "'");
   });
 }

@@ -22,6 +22,7 @@ def test_errors_split_validation_and_test():
     pred = np.array([1.1 if "n-1024" in k or "n-4096" in k else 1.3 for k in app])
     e = bench._errors(wl, app, pred, meas)
     assert abs(e["validation_geomean_rel_error"] - 0.1) < 1e-12
+    assert abs(e["validation_mean_rel_error"] - 0.1) < 1e-12
     assert abs(e["test"]["geomean_rel_error_all"] - 0.3) < 1e-12
     assert e["test"]["rows"] == 4
 
@@ -31,10 +32,10 @@ def test_headline_uses_validation_error_only():
     models = {
         # better on test, worse on validation: must NOT win
         "a": {"gpu_reference_fit": {"calibration_geomean_rel_error": 0.01,
-                                    "validation_geomean_rel_error": 0.20,
+                                    "validation_mean_rel_error": 0.20,
                                     "test": {"geomean_rel_error_all": 0.01}}},
         "b": {"gpu_multistart_fit": {"calibration_geomean_rel_error": 0.05,
-                                     "validation_geomean_rel_error": 0.10,
+                                     "validation_mean_rel_error": 0.10,
                                      "test": {"geomean_rel_error_all": 0.40}}},
         "c": {"gpu_multistart_fit": {"error": "diverged"}},
     }
@@ -87,3 +88,18 @@ def test_per_variant_selection_ranks_first_then_error_on_validation_only():
                                "matmul_sq_prefetch-False": "b/gpu_multistart_fit"}
     assert r["validation_ranking_correct_gap_ge_2pct"] == "2/2"
     assert r["test"]["geomean_rel_error"]["matmul_sq_prefetch-False"] > 1.0
+
+
+def test_selection_mean_is_not_fooled_by_one_exact_row():
+    import bench
+    wl, app = _app()
+    meas = np.ones(len(app))
+    # validation rows n=1024/4096: a is exact on two rows and 40% off on two;
+    # b is 5% off on all four. The geomean prefers a, the mean prefers b.
+    val = [i for i, k in enumerate(app) if "n-1024" in k or "n-4096" in k]
+    pa, pb = np.ones(len(app)), np.full(len(app), 1.05)
+    pa[val[0]] = pa[val[1]] = 1.0 + 1e-9
+    pa[val[2]] = pa[val[3]] = 1.4
+    ea, eb = bench._errors(wl, app, pa, meas), bench._errors(wl, app, pb, meas)
+    assert ea["validation_geomean_rel_error"] < eb["validation_geomean_rel_error"]
+    assert ea["validation_mean_rel_error"] > eb["validation_mean_rel_error"]
