@@ -1072,9 +1072,10 @@ def run_ours(args, dist: Dist) -> None:
     # a short kernel gets one untimed launch before its trials: the first
     # launch after a switch of kernel pays the switch (code fetch, cold
     # L2/TLB, ~2-4 us), which the paper's back-to-back trials after warm-up
-    # never see; for kernels above 2 ms that is < 0.2% and the extra launch
-    # would only lengthen the step
-    warm = {i: 1 if est[i] < 2e-3 else 0 for i in per_kernel}
+    # never see; above 200 us it is < 2% of one trial (< 0.5% of the mean of
+    # a step's four) while the extra launches would lengthen the step (3% at
+    # a 2 ms threshold)
+    warm = {i: 1 if est[i] < 2e-4 else 0 for i in per_kernel}
     # launches of the timed sweep: trials + warm-ups + one queue-ahead kernel
     # per ps_measure call
     sweep_launches = args.steps * sum(cnt + warm[i] + 1 for i, cnt in per_kernel.items())
