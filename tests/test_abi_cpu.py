@@ -63,3 +63,18 @@ def test_init_without_gpu_fails_loudly():
     rc = _abi.lib().ps_init(0, C.byref(ctx))
     assert rc != 0
     assert _abi.lib().ps_last_error()
+
+
+def test_process_options_validate_their_values():
+    import pytest as _pytest
+
+    from paper_1904_09538_b200 import PsError, host
+    for key, good in (("measure_queue_ahead", ("off", "on")),
+                      ("launch_geometry", ("literal", "realised")),
+                      ("partial_subgroups", ("round_up", "strict"))):
+        for v in good:
+            host.set_option(key, v)
+        with _pytest.raises(PsError):
+            host.set_option(key, "sometimes")
+    with _pytest.raises(PsError):
+        host.set_option("no_such_option", "on")
