@@ -164,23 +164,63 @@ int eval_tables_gpu(Ctx* c, const FlatTables& h, const int64_t* points, int64_t 
   double* dpred = reinterpret_cast<double*>(base + off);
   off += (pred_bytes + 255) & ~size_t(255);
   uint8_t* darg = reinterpret_cast<uint8_t*>(base + off);
-  cudaMemcpyAsync(dpts, points, pts_bytes, cudaMemcpyHostToDevice, c->stream);
-  if ((rc = events(c, 2))) return rc;
   const int threads = 128;
-  const int64_t want = (npts + threads - 1) / threads;
-  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->sm_count * 16));
-  cudaEventRecord(c->ev[0], c->stream);
-  eval_points_kernel<<<blocks, threads, 0, c->stream>>>(d, dpts, npts, dpred, darg);
-  cudaEventRecord(c->ev[1], c->stream);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "eval launch failed: %s", cudaGetErrorString(e));
-  cudaMemcpyAsync(pred, dpred, pred_bytes, cudaMemcpyDeviceToHost, c->stream);
-  cudaMemcpyAsync(argmin, darg, arg_bytes, cudaMemcpyDeviceToHost, c->stream);
-  e = cudaStreamSynchronize(c->stream);
+  const int64_t wave = (int64_t)c->sm_count * threads * 8;  // points one chunk launch covers
+  // Chunked pipeline: the points of chunk i+1 copy in (h2d stream) while
+  // chunk i evaluates (context stream) and chunk i-1's predictions copy out
+  // (d2h stream) — the two copy engines and the SMs overlap, so an
+  // end-to-end call costs about max(kernel, copy-out) instead of their sum.
+  // Each chunk is a whole number of 8-CTA-per-SM waves; kernel_seconds is the
+  // sum of the chunk kernels' own event times.
+  const int64_t chunk = npts >= 3 * wave ? std::max<int64_t>(wave, (npts / 6 + wave - 1) / wave * wave) : npts;
+  const int nchunks = (int)((npts + chunk - 1) / chunk);
+  if ((rc = events(c, 1 + 3 * nchunks))) return rc;
+  if (nchunks > 1) {
+    if (!c->h2d_stream && cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return set_error(PS_ERR_CUDA, "stream creation failed");
+    if (!c->d2h_stream && cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return set_error(PS_ERR_CUDA, "stream creation failed");
+    // the copy streams start after everything already on the context stream
+    cudaEventRecord(c->ev[0], c->stream);
+    cudaStreamWaitEvent(c->h2d_stream, c->ev[0], 0);
+    cudaStreamWaitEvent(c->d2h_stream, c->ev[0], 0);
+  }
+  cudaStream_t in_st = nchunks > 1 ? c->h2d_stream : c->stream;
+  cudaStream_t out_st = nchunks > 1 ? c->d2h_stream : c->stream;
+  for (int i = 0; i < nchunks; ++i) {
+    const int64_t lo = (int64_t)i * chunk, n = std::min<int64_t>(chunk, npts - lo);
+    cudaEvent_t in_done = c->ev[1 + 3 * i], k0 = c->ev[2 + 3 * i], k1 = c->ev[3 + 3 * i];
+    cudaMemcpyAsync(dpts + 4 * lo, points + 4 * lo, sizeof(int64_t) * 4 * (size_t)n, cudaMemcpyHostToDevice,
+                    in_st);
+    if (nchunks > 1) {
+      cudaEventRecord(in_done, in_st);
+      cudaStreamWaitEvent(c->stream, in_done, 0);
+    }
+    const unsigned blocks =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, (int64_t)c->sm_count * 16));
+    cudaEventRecord(k0, c->stream);
+    eval_points_kernel<<<blocks, threads, 0, c->stream>>>(d, dpts + 4 * lo, n, dpred + (size_t)lo * h.nvar,
+                                                          darg + (size_t)lo * h.ngroups);
+    cudaEventRecord(k1, c->stream);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "eval launch failed: %s", cudaGetErrorString(e));
+    if (nchunks > 1) cudaStreamWaitEvent(out_st, k1, 0);
+    cudaMemcpyAsync(pred + (size_t)lo * h.nvar, dpred + (size_t)lo * h.nvar, sizeof(double) * (size_t)n * h.nvar,
+                    cudaMemcpyDeviceToHost, out_st);
+    cudaMemcpyAsync(argmin + (size_t)lo * h.ngroups, darg + (size_t)lo * h.ngroups, (size_t)n * h.ngroups,
+                    cudaMemcpyDeviceToHost, out_st);
+  }
+  cudaError_t e = cudaStreamSynchronize(out_st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess && nchunks > 1) e = cudaStreamSynchronize(in_st);
   if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "eval failed: %s", cudaGetErrorString(e));
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
-  if (kernel_seconds) *kernel_seconds = ms * 1e-3;
+  double secs = 0.0;
+  for (int i = 0; i < nchunks; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[2 + 3 * i], c->ev[3 + 3 * i]);
+    secs += ms * 1e-3;
+  }
+  if (kernel_seconds) *kernel_seconds = secs;
   return PS_OK;
 }
 

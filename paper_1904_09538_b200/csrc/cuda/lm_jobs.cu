@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "libm_glibc.cuh"
@@ -61,10 +62,14 @@ struct DevJob {
   int first_cta;
 };
 
-// out[0..n_outputs) = the program's expressions at (p, f).
+// Runs the program at (p, f); its registers live at s[slot * stride]:
+// shared memory (stride = blockDim.x, one column per thread) when the CTA
+// has room, else the thread's local array (stride 1). The results stay in
+// the slots named by pr.outputs.
+template <int kStride>
 __device__ __forceinline__ void exec_program(const DevProgram& pr, const double* __restrict__ p,
-                                             const double* __restrict__ f, double* out) {
-  double s[kJobMaxSlots];
+                                             const double* __restrict__ f, double* s, int stride) {
+  const int st = kStride ? kStride : stride;
   for (int i = 0; i < pr.n_insns; ++i) {
     const uint32_t w0 = __ldg(pr.insns + 2 * i), w1 = __ldg(pr.insns + 2 * i + 1);
     const int op = int(w0 >> 16), d = int(w0 & 0xffff), a = int(w1 >> 16), b = int(w1 & 0xffff);
@@ -73,15 +78,14 @@ __device__ __forceinline__ void exec_program(const DevProgram& pr, const double*
       case PS_BC_NUM: v = __ldg(pr.consts + a); break;
       case PS_BC_PARAM: v = p[a]; break;
       case PS_BC_FEAT: v = f[a]; break;
-      case PS_BC_TANH: v = glibc_tanh(s[a]); break;
-      case PS_BC_ADD: v = __dadd_rn(s[a], s[b]); break;
-      case PS_BC_SUB: v = __dsub_rn(s[a], s[b]); break;
-      case PS_BC_MUL: v = __dmul_rn(s[a], s[b]); break;
-      default: v = __ddiv_rn(s[a], s[b]);
+      case PS_BC_TANH: v = glibc_tanh(s[a * st]); break;
+      case PS_BC_ADD: v = __dadd_rn(s[a * st], s[b * st]); break;
+      case PS_BC_SUB: v = __dsub_rn(s[a * st], s[b * st]); break;
+      case PS_BC_MUL: v = __dmul_rn(s[a * st], s[b * st]); break;
+      default: v = __ddiv_rn(s[a * st], s[b * st]);
     }
-    s[d] = v;
+    s[d * st] = v;
   }
-  for (int k = 0; k < pr.n_outputs; ++k) out[k] = s[pr.outputs[k]];
 }
 
 struct Fit {
@@ -89,13 +93,17 @@ struct Fit {
   const double* f;  // [nr][nf]
   const double* t;  // [nr]
   double* w;        // [nr][np + 1]: scaled J row, then the residual
+  double* slots;    // program registers in shared memory ([slot][thread]) or null
   int np, nr, stride;
   bool ordered, relative;
 };
 
 // Residuals (and, with jacobian, the scaled Jacobian) of every row.
 __device__ void rows_eval(const Fit& F, const double* p, const double* scale, bool jacobian) {
-  double out[kJobMaxParams + 1];
+  double local[kJobMaxSlots];
+  const DevProgram& pr = jacobian ? F.J->full : F.J->value;
+  double* s = F.slots ? F.slots + threadIdx.x : local;
+  const int stride = F.slots ? (int)blockDim.x : 1;
   for (int k = threadIdx.x; k < F.nr; k += blockDim.x) {
     const double* fk = F.f + (size_t)k * F.J->nf;
     double* wk = F.w + (size_t)k * F.stride;
@@ -103,10 +111,14 @@ __device__ void rows_eval(const Fit& F, const double* p, const double* scale, bo
     // applied to the model; see lm.cu)
     const double tk = F.t[k];
     const double w_row = F.relative ? 1.0 / tk : 1.0;
-    exec_program(jacobian ? F.J->full : F.J->value, p, fk, out);
-    wk[F.np] = __dmul_rn(__dsub_rn(tk, out[0]), w_row);
+    if (F.slots)
+      exec_program<0>(pr, p, fk, s, stride);
+    else
+      exec_program<1>(pr, p, fk, s, 1);
+    wk[F.np] = __dmul_rn(__dsub_rn(tk, s[pr.outputs[0] * stride]), w_row);
     if (jacobian)
-      for (int i = 0; i < F.np; ++i) wk[i] = __dmul_rn(__dmul_rn(out[1 + i], scale[i]), w_row);
+      for (int i = 0; i < F.np; ++i)
+        wk[i] = __dmul_rn(__dmul_rn(s[pr.outputs[1 + i] * stride], scale[i]), w_row);
   }
   __syncthreads();
 }
@@ -195,7 +207,8 @@ __device__ int warp_solve(int np, const double* jtj, const double* jtr, double l
   return 0;
 }
 
-__global__ void __launch_bounds__(kJobThreads) lm_jobs_kernel(const DevJob* __restrict__ jobs, int njobs) {
+__global__ void __launch_bounds__(kJobThreads) lm_jobs_kernel(const DevJob* __restrict__ jobs, int njobs,
+                                                              size_t rows_bytes, int slots_in_smem) {
   // the job of this CTA: the last job whose first CTA is <= blockIdx.x
   int lo = 0, hi = njobs - 1;
   while (lo < hi) {
@@ -223,6 +236,8 @@ __global__ void __launch_bounds__(kJobThreads) lm_jobs_kernel(const DevJob* __re
   F.f = J.features + (J.shared_rows ? 0 : (size_t)b * J.nr * J.nf);
   F.t = J.t + (J.shared_rows ? 0 : (size_t)b * J.nr);
   F.w = J.work ? J.work + (size_t)b * J.nr * F.stride : smem;
+  // program registers after the J rows (dynamic shared memory), when they fit
+  F.slots = slots_in_smem ? smem + rows_bytes / sizeof(double) : nullptr;
   F.ordered = (J.mode & 2) == 0;
   F.relative = (J.mode & 4) != 0;
   const ps_fit_opts& opt = J.opt;
@@ -438,13 +453,21 @@ int fit_lm_jobs_gpu(Ctx* c, int njobs, const LmJobHost* jobs, double* kernel_sec
     ctas += h.nbatch;
   }
   DevJob* djobs = static_cast<DevJob*>(up(dj.data(), sizeof(DevJob) * njobs));
-  const size_t dyn = rows_in_smem ? rows_bytes : 0;
+  const size_t rows_dyn = rows_in_smem ? rows_bytes : 0;
+  // program registers in shared memory ([slot][thread], every thread its
+  // column) when they fit beside the J rows: the interpreter's operand
+  // traffic stays on chip instead of in local memory
+  int max_slots = 1;
+  for (int j = 0; j < njobs; ++j) max_slots = std::max({max_slots, jobs[j].full.n_slots, jobs[j].value.n_slots});
+  const size_t slots_bytes = sizeof(double) * (size_t)max_slots * kJobThreads;
+  const bool slots_in_smem = rows_dyn + slots_bytes <= smem_cap && !std::getenv("PS_LM_LOCAL_SLOTS");
+  const size_t dyn = rows_dyn + (slots_in_smem ? slots_bytes : 0);
   // static + dynamic above 48 KB needs the opt-in limit raised
   if (cudaFuncSetAttribute(lm_jobs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess)
     return set_error(PS_ERR_CUDA, "LM jobs: cannot reserve %zu B of shared memory", dyn);
   if ((rc = events(c, 2))) return rc;
   cudaEventRecord(c->ev[0], c->stream);
-  lm_jobs_kernel<<<ctas, kJobThreads, dyn, c->stream>>>(djobs, njobs);
+  lm_jobs_kernel<<<ctas, kJobThreads, dyn, c->stream>>>(djobs, njobs, rows_dyn, slots_in_smem ? 1 : 0);
   cudaEventRecord(c->ev[1], c->stream);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "LM jobs launch failed: %s", cudaGetErrorString(e));
