@@ -456,10 +456,12 @@ def model_reports(parts, mean_s: dict[str, float], dev=None) -> tuple[dict, dict
         wall = time.perf_counter() - t0
         nfits = sum(len(j["starts"]) for j in jobs)
         iters = sum(s["iterations"] for _, st in results for s in st)
+        damped = sum(s.get("trials", 0) for _, st in results for s in st)
         k17 = {"jobs": len(jobs), "fits": nfits, "launches": 1, "kernel_s": round(ksec, 5),
                "first_launch_s": round(first_s, 5) if first_s is not None else None,
                "wall_s": round(wall, 4), "fits_per_s": round(nfits / ksec, 1),
-               "lm_iterations": iters, "iterations_per_s": round(iters / ksec, 1)}
+               "lm_iterations": iters, "damped_solves": damped,
+               "iterations_per_s": round(iters / ksec, 1)}
         for (wl, mname, key), (params, stats) in zip(where, results):
             m, p_ref, tc, ta, cal, app = prep[(wl.name, mname)]
             ok = [i for i, s_ in enumerate(stats) if s_["status"] == 0]

@@ -227,7 +227,7 @@ typedef struct ps_fit_stats {
   int32_t iterations;
   int32_t converged;
   int32_t status;        /* 0 ok, 1 damping overflow (divergence) */
-  int32_t reserved;
+  int32_t trials;        /* damped solves tried (K17 v2; 0 elsewhere) */
 } ps_fit_stats;
 
 /* Batched LM: `nbatch` independent fits of one model (np params, nf

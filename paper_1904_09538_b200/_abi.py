@@ -57,7 +57,7 @@ class FitOpts(C.Structure):
 
 class FitStats(C.Structure):
     _fields_ = [("residual_norm", C.c_double), ("iterations", C.c_int32),
-                ("converged", C.c_int32), ("status", C.c_int32), ("reserved", C.c_int32)]
+                ("converged", C.c_int32), ("status", C.c_int32), ("trials", C.c_int32)]
 
 
 class PsError(RuntimeError):

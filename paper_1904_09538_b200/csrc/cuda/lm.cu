@@ -350,6 +350,7 @@ __global__ void __launch_bounds__(kLmThreads) lm_batched_kernel(LmArgs A) {
     A.stats[b].iterations = iter;
     A.stats[b].converged = converged;
     A.stats[b].status = status;
+    A.stats[b].trials = 0;
   }
 }
 

@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kJobThreads) lm_jobs_kernel(const DevJob* __re
   rows_eval(F, p, scale, false);
   double cost = cost_of(F, &red);
   double lambda = opt.lambda0;
-  int iter = 0, converged = 0, status = 0;
+  int iter = 0, converged = 0, status = 0, trials = 0;
   if (!isfinite(cost)) status = 3;
 
   for (; !status && iter < opt.max_iterations; ++iter) {
@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(kJobThreads) lm_jobs_kernel(const DevJob* __re
     }
     bool accepted = false;
     while (!accepted) {
+      ++trials;
       if (warp == 0) {
         int fl = 0;
         if (lambda > 1e100) {
@@ -361,6 +362,7 @@ __global__ void __launch_bounds__(kJobThreads) lm_jobs_kernel(const DevJob* __re
     J.stats[b].iterations = iter;
     J.stats[b].converged = converged;
     J.stats[b].status = status;
+    J.stats[b].trials = trials;
   }
 }
 

@@ -152,6 +152,7 @@ int ps_fit_cpu(const char* model_text, const double* features, const double* t, 
       stats->iterations = cm.iterations;
       stats->converged = cm.converged ? 1 : 0;
       stats->status = 0;
+      stats->trials = 0;
     }
     return PS_OK;
   });

@@ -261,6 +261,7 @@ def fit_lm_jobs(dev: CudaDevice, jobs: list[dict]):
     secs = C.c_double()
     check(L.ps_fit_lm_jobs(dev._ctx, len(jobs), arr, C.byref(secs)))
     res = [(p, [{"residual_norm": s.residual_norm, "iterations": s.iterations,
-                 "converged": bool(s.converged), "status": s.status} for s in st])
+                 "converged": bool(s.converged), "status": s.status, "trials": s.trials}
+                for s in st])
            for p, st in outs]
     return res, secs.value

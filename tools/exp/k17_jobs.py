@@ -53,7 +53,7 @@ with CudaDevice(0) as dev:
         r, s = fit_lm_jobs(dev, [job])
         its = [st["iterations"] for st in r[0][1]]
         out.append((s, name, len(job["starts"]), job["features"].shape, its,
-                    [st["status"] for st in r[0][1]]))
+                    [st["trials"] for st in r[0][1]]))
     for s, name, nb, shape, its, stat in sorted(out, reverse=True):
         print(f"  {s * 1e3:9.3f} ms  {name:28s} starts {nb}  rows x feats {shape}  "
-              f"iterations {its} status {stat}")
+              f"iterations {its} damped trials {stat}")
