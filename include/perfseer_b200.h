@@ -286,6 +286,17 @@ int ps_tables_info(const ps_tables* tables, int* nvar, int* ngroups, int64_t* nt
 int ps_tables_free(ps_tables* tables);
 int ps_eval_batched(ps_ctx* ctx, const ps_tables* tables, const int64_t* points, int64_t npts,
                     double* pred, uint8_t* argmin, double* kernel_seconds);
+/* K18 specialised to one table set: the tables' feature polynomials and
+ * model programs as one kernel compiled at run time (NVRTC, sm_100a) and
+ * cached per device — what ps_eval_batched launches unless the option
+ * "k18_jit" is off (then the table interpreter). ps_eval_prepare compiles
+ * and loads it ahead of the first evaluation (jit_seconds: the time this
+ * call spent); ps_eval_jit_source returns the generated CUDA source;
+ * ps_eval_jit_compile compiles it without a device (cubin size out). Same
+ * bits as the interpreter and ps_eval_cpu. */
+int ps_eval_prepare(ps_ctx* ctx, const ps_tables* tables, double* jit_seconds);
+int ps_eval_jit_source(const ps_tables* tables, char* out, size_t cap, size_t* needed);
+int ps_eval_jit_compile(const ps_tables* tables, size_t* cubin_bytes);
 /* The same evaluation on `threads` host threads (CPU port of K18). */
 int ps_eval_cpu(const ps_tables* tables, const int64_t* points, int64_t npts, double* pred,
                 uint8_t* argmin, int threads);
@@ -345,6 +356,8 @@ int ps_model_program(const char* model_text, int with_jacobian, char* out, size_
  * (ceil(wg/32) sub-groups); "launch_geometry" = realised
  * (vectorised row sweeps, FD strips) | literal (one CTA per IR work-group,
  * the grid/block of launch_geometry, transforms.cpp:242-275);
+ * "k18_jit" = on (default: ps_eval_batched runs the tables' run-time
+ * specialised kernel) | off (the table interpreter);
  * "measure_queue_ahead" = on (default: ps_measure enqueues a short idle
  * kernel before the timed trials so each event pair brackets device work
  * only, like the OpenCL profiling timestamps the paper reads) | off. */

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(128) eval_points_kernel(FlatTables t, const in
 }
 
 int eval_tables_gpu(Ctx* c, const FlatTables& h, const int64_t* points, int64_t npts, double* pred,
-                    uint8_t* argmin, double* kernel_seconds) {
+                    uint8_t* argmin, double* kernel_seconds, void* jit_kernel) {
   if (h.ngroups > kEvalMaxGroups) return set_error(PS_ERR_ARG, "at most %d application groups", kEvalMaxGroups);
   if (h.nvar > kEvalMaxVariants) return set_error(PS_ERR_ARG, "at most %d variants", kEvalMaxVariants);
   for (int m = 0; m < h.nmodels; ++m) {
@@ -199,8 +199,18 @@ int eval_tables_gpu(Ctx* c, const FlatTables& h, const int64_t* points, int64_t 
     const unsigned blocks =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, (int64_t)c->sm_count * 16));
     cudaEventRecord(k0, c->stream);
-    eval_points_kernel<<<blocks, threads, 0, c->stream>>>(d, dpts + 4 * lo, n, dpred + (size_t)lo * h.nvar,
-                                                          darg + (size_t)lo * h.ngroups);
+    if (jit_kernel) {  // the tables compiled into one kernel (eval_jit.cu)
+      const int64_t* kp = dpts + 4 * lo;
+      double* kpred = dpred + (size_t)lo * h.nvar;
+      uint8_t* karg = darg + (size_t)lo * h.ngroups;
+      const double* kparams = d.params;
+      int64_t kn = n;
+      void* args[] = {&kp, &kn, &kpred, &karg, &kparams};
+      cudaLaunchKernel(jit_kernel, dim3(blocks), dim3(threads), args, 0, c->stream);
+    } else {
+      eval_points_kernel<<<blocks, threads, 0, c->stream>>>(d, dpts + 4 * lo, n, dpred + (size_t)lo * h.nvar,
+                                                            darg + (size_t)lo * h.ngroups);
+    }
     cudaEventRecord(k1, c->stream);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_error(PS_ERR_CUDA, "eval launch failed: %s", cudaGetErrorString(e));

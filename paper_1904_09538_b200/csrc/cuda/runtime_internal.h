@@ -126,6 +126,13 @@ void set_literal_geometry(bool on);
 bool literal_geometry();
 // Queue-ahead kernel before ps_measure's timed trials (on by default).
 void set_queue_ahead(bool on);
+// K18 run-time specialisation (eval_jit.cu): the tables as one NVRTC-compiled
+// kernel (on by default; off = the table interpreter in eval.cu).
+void set_k18_jit(bool on);
+bool k18_jit_enabled();
+std::string k18_jit_source(const struct FlatTables& h);
+int k18_jit_compile(const std::string& src, std::vector<char>* cubin);
+int k18_jit_kernel(Ctx* c, const struct FlatTables& h, void** kernel, double* compile_seconds);
 
 // K17 v2 (lm_jobs.cu): straight-line model programs (host-compiled,
 // perfseer::compile_program) and one fit job per (model, problem, starts).
@@ -146,7 +153,9 @@ struct LmJobHost {
 };
 int fit_lm_jobs_gpu(Ctx* c, int njobs, const LmJobHost* jobs, double* kernel_seconds);
 
+// jit_kernel: the tables' specialised kernel (k18_jit_kernel), or null for
+// the table interpreter
 int eval_tables_gpu(Ctx* c, const FlatTables& t, const int64_t* points, int64_t npts, double* pred,
-                    uint8_t* argmin, double* kernel_seconds);
+                    uint8_t* argmin, double* kernel_seconds, void* jit_kernel = nullptr);
 
 }  // namespace ps

@@ -285,6 +285,11 @@ int ps_set_option(const char* key, const char* value) {
       ps::set_literal_geometry(v == "literal");
       return PS_OK;
     }
+    if (k == "k18_jit") {
+      if (v != "on" && v != "off") throw EvalError("k18_jit: on | off");
+      ps::set_k18_jit(v == "on");
+      return PS_OK;
+    }
     if (k == "measure_queue_ahead") {
       if (v != "on" && v != "off") throw EvalError("measure_queue_ahead: on | off");
       ps::set_queue_ahead(v == "on");
@@ -317,6 +322,8 @@ struct ps_tables {
   std::vector<uint32_t> insns;
   std::vector<double> consts, params;
   std::vector<int8_t> term_exp;
+  // K18 kernels specialised to these tables (eval_jit.cu), per device
+  mutable std::map<int, void*> jit;
   ps::FlatTables flat() const {
     ps::FlatTables f{};
     f.nvar = int(t.var_model.size());
@@ -390,11 +397,51 @@ int ps_tables_free(ps_tables* t) {
   return PS_OK;
 }
 
+// The tables' specialised K18 kernel on ctx's device (compiled and loaded on
+// first use), or null when the interpreter is selected.
+static int jit_kernel_for(ps_ctx* ctx, const ps_tables* tables, void** kernel, double* seconds) {
+  *kernel = nullptr;
+  if (seconds) *seconds = 0.0;
+  if (!ps::k18_jit_enabled()) return PS_OK;
+  auto* c = reinterpret_cast<ps::Ctx*>(ctx);
+  auto it = tables->jit.find(c->device);
+  if (it != tables->jit.end()) {
+    *kernel = it->second;
+    return PS_OK;
+  }
+  const int rc = ps::k18_jit_kernel(c, tables->flat(), kernel, seconds);
+  if (rc == PS_OK) tables->jit[c->device] = *kernel;
+  return rc;
+}
+
+int ps_eval_prepare(ps_ctx* ctx, const ps_tables* tables, double* jit_seconds) {
+  if (!ctx || !tables) return ps::set_error(PS_ERR_ARG, "ps_eval_prepare: null argument");
+  void* k = nullptr;
+  return jit_kernel_for(ctx, tables, &k, jit_seconds);
+}
+
+int ps_eval_jit_source(const ps_tables* tables, char* out, size_t cap, size_t* needed) {
+  return guarded([&] {
+    if (!tables) throw EvalError("ps_eval_jit_source: null tables");
+    return copy_out(ps::k18_jit_source(tables->flat()), out, cap, needed);
+  });
+}
+
+int ps_eval_jit_compile(const ps_tables* tables, size_t* cubin_bytes) {
+  if (!tables) return ps::set_error(PS_ERR_ARG, "ps_eval_jit_compile: null tables");
+  std::vector<char> cubin;
+  const int rc = ps::k18_jit_compile(ps::k18_jit_source(tables->flat()), &cubin);
+  if (rc == PS_OK && cubin_bytes) *cubin_bytes = cubin.size();
+  return rc;
+}
+
 int ps_eval_batched(ps_ctx* ctx, const ps_tables* tables, const int64_t* points, int64_t npts,
                     double* pred, uint8_t* argmin, double* kernel_seconds) {
   if (!ctx || !tables || !points || !pred || !argmin) return ps::set_error(PS_ERR_ARG, "ps_eval_batched: null argument");
+  void* jit = nullptr;
+  if (int rc = jit_kernel_for(ctx, tables, &jit, nullptr)) return rc;
   return ps::eval_tables_gpu(reinterpret_cast<ps::Ctx*>(ctx), tables->flat(), points, npts, pred, argmin,
-                             kernel_seconds);
+                             kernel_seconds, jit);
 }
 
 // The same evaluation on host threads (exact int128 features, double model).

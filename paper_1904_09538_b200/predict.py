@@ -28,8 +28,11 @@ def _declare():
                                   _P(C.c_double), _P(C.c_uint8), _P(C.c_double)]
     L.ps_eval_cpu.argtypes = [C.c_void_p, _P(C.c_int64), C.c_int64, _P(C.c_double),
                               _P(C.c_uint8), C.c_int]
+    L.ps_eval_prepare.argtypes = [C.c_void_p, C.c_void_p, _P(C.c_double)]
+    L.ps_eval_jit_source.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t, _P(C.c_size_t)]
+    L.ps_eval_jit_compile.argtypes = [C.c_void_p, _P(C.c_size_t)]
     for n in ("ps_tables_build", "ps_tables_info", "ps_tables_free", "ps_eval_batched",
-              "ps_eval_cpu"):
+              "ps_eval_cpu", "ps_eval_prepare", "ps_eval_jit_source", "ps_eval_jit_compile"):
         getattr(L, n).restype = C.c_int
     L._k18_declared = True
     return L
@@ -82,6 +85,28 @@ class PredictionTables:
         pred = bufs[1].numpy(np.float64)[: npts * self.nvar].reshape(npts, self.nvar)
         arg = bufs[2].numpy(np.uint8)[: npts * self.ngroups].reshape(npts, self.ngroups)
         return pts, pred, arg, bufs
+
+    def prepare_gpu(self, dev) -> float:
+        """Compile and load the tables' specialised K18 kernel on dev ahead of
+        the first evaluation (NVRTC); returns the seconds this call spent (0
+        when it was already loaded, or with the option k18_jit off)."""
+        secs = C.c_double()
+        check(_declare().ps_eval_prepare(dev._ctx, self._h, C.byref(secs)))
+        return secs.value
+
+    def jit_source(self) -> str:
+        """The CUDA source of the tables' specialised kernel."""
+        L, need = _declare(), C.c_size_t()
+        L.ps_eval_jit_source(self._h, None, 0, C.byref(need))  # size query
+        buf = C.create_string_buffer(need.value + 1)
+        check(L.ps_eval_jit_source(self._h, buf, len(buf), C.byref(need)))
+        return buf.value.decode()
+
+    def jit_compile(self) -> int:
+        """Compile the specialised kernel with NVRTC (no device); cubin bytes."""
+        n = C.c_size_t()
+        check(_declare().ps_eval_jit_compile(self._h, C.byref(n)))
+        return n.value
 
     def eval_gpu(self, dev, points: np.ndarray, out=None):
         """K18 on dev. out = (pred, argmin) writes into caller buffers (e.g.

@@ -120,3 +120,20 @@ def test_literal_launch_geometry_matches_oracle(dev, variant_id):
         host.set_option("launch_geometry", "realised")
     for g, w in zip(got, oracle_suite.run(d, io, ins)):
         np.testing.assert_array_equal(g.view(np.uint8), w.view(np.uint8), err_msg=variant_id)
+
+
+GOLDEN = __import__("json").loads(
+    (__import__("pathlib").Path(__file__).parent / "golden" / "reference.json").read_text())
+
+
+@pytest.mark.parametrize("case", GOLDEN["kernels"], ids=lambda c: c["id"])
+def test_kernel_matches_reference_interpreter(dev, case):
+    """The CUDA kernel against the REFERENCE's own IR interpreter
+    (run_reference, tests/support.hpp:50-162, via oracle/gen_golden.cpp) on
+    its seed-pattern inputs — no restatement in between. DG (and matmul PF)
+    are pinned to the untiled source kernel the interpreter can run."""
+    d, io = desc_io(case["id"])
+    got = dev.run(d, make_inputs(d, io, "seed17"))
+    expect = np.asarray(case["values"], dtype=np.float64)
+    assert got[0].size == expect.size
+    np.testing.assert_array_equal(got[0].astype(np.float64), expect)

@@ -97,3 +97,21 @@ def test_gpu_eval_chunked_pipeline_matches_cpu(dev):
     g1, a1, _ = t.eval_gpu(dev, pts[:100_000])
     np.testing.assert_array_equal(g[:100_000].view(np.uint64), np.asarray(g1).view(np.uint64))
     assert np.array_equal(a[:100_000], np.asarray(a1))
+
+
+def test_jit_kernel_matches_interpreter_bitwise(dev):
+    """The run-time specialised K18 kernel (default) against the table
+    interpreter (option k18_jit off) on the same points: identical bits."""
+    from paper_1904_09538_b200 import host
+    from paper_1904_09538_b200.predict import c5_points
+    t, _ = _tables()
+    pts = c5_points(300_000, seed=9)
+    assert t.prepare_gpu(dev) >= 0.0
+    gj, aj, _ = t.eval_gpu(dev, pts)
+    host.set_option("k18_jit", "off")
+    try:
+        gi, ai, _ = t.eval_gpu(dev, pts)
+    finally:
+        host.set_option("k18_jit", "on")
+    np.testing.assert_array_equal(np.asarray(gj).view(np.uint64), np.asarray(gi).view(np.uint64))
+    assert np.array_equal(np.asarray(aj), np.asarray(ai))
