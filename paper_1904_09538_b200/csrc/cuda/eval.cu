@@ -125,7 +125,12 @@ int eval_tables_gpu(Ctx* c, const FlatTables& h, const int64_t* points, int64_t 
     void** dst;
   };
   FlatTables d = h;
-  std::vector<Part> parts = {
+  std::vector<Part> parts;
+  if (jit_kernel) {
+    // the specialised kernel carries the tables in its code: only the
+    // fitted parameters travel
+    parts = {{h.params, sizeof(double) * h.model_param_begin[h.nmodels], (void**)&d.params}};
+  } else parts = {
       {h.var_group, sizeof(int32_t) * h.nvar, (void**)&d.var_group},
       {h.var_model, sizeof(int32_t) * h.nvar, (void**)&d.var_model},
       {h.var_feat_base, sizeof(int32_t) * h.nvar, (void**)&d.var_feat_base},
@@ -172,7 +177,7 @@ int eval_tables_gpu(Ctx* c, const FlatTables& h, const int64_t* points, int64_t 
   // end-to-end call costs about max(kernel, copy-out) instead of their sum.
   // Each chunk is a whole number of 8-CTA-per-SM waves; kernel_seconds is the
   // sum of the chunk kernels' own event times.
-  const int64_t chunk = npts >= 3 * wave ? std::max<int64_t>(wave, (npts / 6 + wave - 1) / wave * wave) : npts;
+  const int64_t chunk = npts >= 3 * wave ? std::max<int64_t>(wave, (npts / 8 + wave - 1) / wave * wave) : npts;
   const int nchunks = (int)((npts + chunk - 1) / chunk);
   if ((rc = events(c, 1 + 3 * nchunks))) return rc;
   if (nchunks > 1) {
