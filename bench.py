@@ -832,7 +832,8 @@ def c5_report(dev, parts, variants: list[dict], npts: int = 1_000_000, dist=None
         # the tables' specialised kernel (NVRTC), compiled and loaded before
         # the timed call; the seconds are reported, not hidden
         jit_s = t.prepare_gpu(dev)
-        t.eval_gpu(dev, pts[lo:lo + max(1, min(4096, hi - lo))])  # warm
+        # warm at the timed size (device buffers, streams and events exist)
+        t.eval_gpu(dev, ppts, out=(ppred, parg))
     except Exception as e:  # every rank learns of it before the collectives
         err = e
     if dist and dist.max(float(err is not None)) > 0:
