@@ -204,14 +204,20 @@ int eval_tables_gpu(Ctx* c, const FlatTables& h, const int64_t* points, int64_t 
     const unsigned blocks =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, (int64_t)c->sm_count * 16));
     cudaEventRecord(k0, c->stream);
-    if (jit_kernel) {  // the tables compiled into one kernel (eval_jit.cu)
+    if (jit_kernel) {  // the tables compiled into kernels (eval_jit.cu)
+      const JitKernels* jk = static_cast<const JitKernels*>(jit_kernel);
       const int64_t* kp = dpts + 4 * lo;
       double* kpred = dpred + (size_t)lo * h.nvar;
       uint8_t* karg = darg + (size_t)lo * h.ngroups;
       const double* kparams = d.params;
       int64_t kn = n;
-      void* args[] = {&kp, &kn, &kpred, &karg, &kparams};
-      cudaLaunchKernel(jit_kernel, dim3(blocks), dim3(threads), args, 0, c->stream);
+      const unsigned bx = std::max(1u, (unsigned)std::min<int64_t>((n + threads - 1) / threads,
+                                                                    (int64_t)c->sm_count * 16));
+      void* pargs[] = {&kp, &kn, &kpred, &kparams};
+      cudaLaunchKernel(reinterpret_cast<const void*>(jk->predict), dim3(bx, (unsigned)h.nvar), dim3(threads),
+                       pargs, 0, c->stream);
+      void* rargs[] = {&kpred, &kn, &karg};
+      cudaLaunchKernel(reinterpret_cast<const void*>(jk->rank), dim3(blocks), dim3(threads), rargs, 0, c->stream);
     } else {
       eval_points_kernel<<<blocks, threads, 0, c->stream>>>(d, dpts + 4 * lo, n, dpred + (size_t)lo * h.nvar,
                                                             darg + (size_t)lo * h.ngroups);

@@ -128,6 +128,10 @@ bool literal_geometry();
 void set_queue_ahead(bool on);
 // K18 run-time specialisation (eval_jit.cu): the tables as one NVRTC-compiled
 // kernel (on by default; off = the table interpreter in eval.cu).
+struct JitKernels {
+  cudaKernel_t predict = nullptr;  // grid.y = variant: pred[pt][v]
+  cudaKernel_t rank = nullptr;     // argmin per group from pred
+};
 void set_k18_jit(bool on);
 bool k18_jit_enabled();
 std::string k18_jit_source(const struct FlatTables& h);
