@@ -70,8 +70,15 @@ template <int kStride>
 __device__ __forceinline__ void exec_program(const DevProgram& pr, const double* __restrict__ p,
                                              const double* __restrict__ f, double* s, int stride) {
   const int st = kStride ? kStride : stride;
-  for (int i = 0; i < pr.n_insns; ++i) {
-    const uint32_t w0 = __ldg(pr.insns + 2 * i), w1 = __ldg(pr.insns + 2 * i + 1);
+  // one 8-byte load per instruction, fetched one instruction ahead so the
+  // fetch latency overlaps the current instruction's operands and operation
+  const uint2* ins = reinterpret_cast<const uint2*>(pr.insns);
+  const int n = pr.n_insns;
+  uint2 next = n > 0 ? __ldg(ins) : make_uint2(0u, 0u);
+  for (int i = 0; i < n; ++i) {
+    const uint2 w = next;
+    if (i + 1 < n) next = __ldg(ins + i + 1);
+    const uint32_t w0 = w.x, w1 = w.y;
     const int op = int(w0 >> 16), d = int(w0 & 0xffff), a = int(w1 >> 16), b = int(w1 & 0xffff);
     double v;
     switch (op) {
