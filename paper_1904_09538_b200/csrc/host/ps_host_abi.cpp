@@ -311,6 +311,7 @@ int ps_geo_mean_rel_error(const double* pred, const double* meas, int n, double*
 // ---------------------------------------------------------------------------
 // K18 tables
 
+#include <mutex>
 #include <thread>
 
 #include "ps_tables.hpp"
@@ -322,8 +323,10 @@ struct ps_tables {
   std::vector<uint32_t> insns;
   std::vector<double> consts, params;
   std::vector<int8_t> term_exp;
-  // K18 kernels specialised to these tables (eval_jit.cu), per device
+  // K18 kernels specialised to these tables (eval_jit.cu), per device; one
+  // table set may be evaluated from several contexts (GPUs) on several threads
   mutable std::map<int, void*> jit;
+  mutable std::mutex jit_mu;
   ps::FlatTables flat() const {
     ps::FlatTables f{};
     f.nvar = int(t.var_model.size());
@@ -404,6 +407,7 @@ static int jit_kernel_for(ps_ctx* ctx, const ps_tables* tables, void** kernel, d
   if (seconds) *seconds = 0.0;
   if (!ps::k18_jit_enabled()) return PS_OK;
   auto* c = reinterpret_cast<ps::Ctx*>(ctx);
+  std::lock_guard<std::mutex> lock(tables->jit_mu);
   auto it = tables->jit.find(c->device);
   if (it != tables->jit.end()) {
     *kernel = it->second;
