@@ -211,7 +211,8 @@ int eval_tables_gpu(Ctx* c, const FlatTables& h, const int64_t* points, int64_t 
       uint8_t* karg = darg + (size_t)lo * h.ngroups;
       const double* kparams = d.params;
       int64_t kn = n;
-      const unsigned bx = std::max(1u, (unsigned)std::min<int64_t>((n + threads - 1) / threads,
+      const int64_t per_cta = (int64_t)threads * jk->lanes;
+      const unsigned bx = std::max(1u, (unsigned)std::min<int64_t>((n + per_cta - 1) / per_cta,
                                                                     (int64_t)c->sm_count * 16));
       void* pargs[] = {&kp, &kn, &kpred, &kparams};
       cudaLaunchKernel(reinterpret_cast<const void*>(jk->predict), dim3(bx, (unsigned)h.nvar), dim3(threads),

@@ -131,6 +131,7 @@ void set_queue_ahead(bool on);
 struct JitKernels {
   cudaKernel_t predict = nullptr;  // grid.y = variant: pred[pt][v]
   cudaKernel_t rank = nullptr;     // argmin per group from pred
+  int lanes = 1;                   // points per thread of predict
 };
 void set_k18_jit(bool on);
 bool k18_jit_enabled();
