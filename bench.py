@@ -1087,10 +1087,12 @@ def run_ours(args, dist: Dist) -> None:
     # launches of the timed sweep: trials + warm-ups + one queue-ahead kernel
     # per ps_measure call
     sweep_launches = args.steps * sum(cnt + warm[i] + 1 for i, cnt in per_kernel.items())
-    for step in range(args.steps):
-        for i, cnt in per_kernel.items():
-            for j, s in enumerate(dev.measure(descs[i], trials=cnt, warmup=warm[i])):
-                records.append((i, step * args.trials_per_step + j, s))
+    from paper_1904_09538_b200.host import trace
+    with trace("bench: timed sweep"):
+        for step in range(args.steps):
+            for i, cnt in per_kernel.items():
+                for j, s in enumerate(dev.measure(descs[i], trials=cnt, warmup=warm[i])):
+                    records.append((i, step * args.trials_per_step + j, s))
     dev.mark(1)
     elapsed = dev.elapsed(0, 1)
     wall = time.perf_counter() - t_wall
@@ -1176,12 +1178,13 @@ def run_ours(args, dist: Dist) -> None:
     dist.barrier()
     e2e_time = e2e_full_time = 0.0
     e2e_bytes = 0.0
-    for _ in range(args.steps):
-        if e2e_set:
-            e2e_time += dev.run_host_batch(batch, b_in, None, checksums=True)[0]
-            if full_outputs:
-                e2e_full_time += dev.run_host_batch(batch, b_in, b_out)
-        e2e_bytes += sum(ios[i].bytes_global for i in e2e_set)
+    with trace("bench: e2e through host buffers"):
+        for _ in range(args.steps):
+            if e2e_set:
+                e2e_time += dev.run_host_batch(batch, b_in, None, checksums=True)[0]
+                if full_outputs:
+                    e2e_full_time += dev.run_host_batch(batch, b_in, b_out)
+            e2e_bytes += sum(ios[i].bytes_global for i in e2e_set)
     e2e_time_max = dist.max(e2e_time)
     e2e_full_time_max = dist.max(e2e_full_time)
     d2h_full = d2h
@@ -1313,7 +1316,8 @@ def run_ours(args, dist: Dist) -> None:
     # the fit runs once (rank 0); its headline parameters go to every rank
     models, heads, k17 = {}, {}, None
     if dist.rank == 0:
-        models, k17 = model_reports(parts, mean_s, dev)
+        with trace("bench: calibration fits (K17)"):
+            models, k17 = model_reports(parts, mean_s, dev)
         for wl, cal, app in parts:
             forced = args.headline_model if args.headline_model in wl.models else ""
             hmodel, hfit, head = headline(models[wl.name], forced)
@@ -1339,8 +1343,9 @@ def run_ours(args, dist: Dist) -> None:
         variants, err = None, str(e)
     variants, err = dist.broadcast((variants, err))
     try:
-        model_eval = (c5_report(dev, parts, variants, args.c5_points, dist)
-                      if args.c5_points and variants else ({"error": err} if err else None))
+        with trace("bench: variant-space prediction (K18)"):
+            model_eval = (c5_report(dev, parts, variants, args.c5_points, dist)
+                          if args.c5_points and variants else ({"error": err} if err else None))
     except Exception as e:  # reported, not hidden
         model_eval = {"error": str(e)}
     if dist.rank != 0:

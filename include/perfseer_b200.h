@@ -362,6 +362,12 @@ int ps_model_program(const char* model_text, int with_jacobian, char* out, size_
  * kernel before the timed trials so each event pair brackets device work
  * only, like the OpenCL profiling timestamps the paper reads) | off. */
 int ps_set_option(const char* key, const char* value);
+/* NVTX ranges for a host pipeline's stages (sweep, e2e, fits, predictions:
+ * visible in nsys / ncu timelines; free without a profiler). The library
+ * opens its own ranges around ps_measure, the e2e batch, K17, K18 and the K18
+ * compile. */
+int ps_trace_push(const char* name);
+int ps_trace_pop(void);
 /* geo_mean_rel_error (executor.cpp:50-61). */
 int ps_geo_mean_rel_error(const double* pred, const double* meas, int n, double* out);
 

@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(128) eval_points_kernel(FlatTables t, const in
 
 int eval_tables_gpu(Ctx* c, const FlatTables& h, const int64_t* points, int64_t npts, double* pred,
                     uint8_t* argmin, double* kernel_seconds, void* jit_kernel) {
+  TraceRange trace(jit_kernel ? "K18 eval (specialised)" : "K18 eval (interpreter)");
   if (h.ngroups > kEvalMaxGroups) return set_error(PS_ERR_ARG, "at most %d application groups", kEvalMaxGroups);
   if (h.nvar > kEvalMaxVariants) return set_error(PS_ERR_ARG, "at most %d variants", kEvalMaxVariants);
   for (int m = 0; m < h.nmodels; ++m) {

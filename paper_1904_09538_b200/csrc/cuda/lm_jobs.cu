@@ -374,6 +374,7 @@ __global__ void __launch_bounds__(kJobThreads) lm_jobs_kernel(const DevJob* __re
 }
 
 int fit_lm_jobs_gpu(Ctx* c, int njobs, const LmJobHost* jobs, double* kernel_seconds) {
+  TraceRange trace("K17 fit_lm_jobs");
   if (njobs < 1) return set_error(PS_ERR_ARG, "ps_fit_lm_jobs: no jobs");
   int dev_smem = 0;
   cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);

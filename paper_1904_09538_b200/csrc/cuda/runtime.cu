@@ -899,6 +899,7 @@ int ps_measure(ps_ctx* ctx, const ps_kernel_desc* desc, int warmup, int trials,
                double* out_seconds) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c || !desc || !out_seconds) return set_error(PS_ERR_ARG, "ps_measure: null argument");
+  TraceRange trace("ps_measure");
   if (trials < 1) return set_error(PS_ERR_ARG, "trials must be >= 1");  // executor.cpp:145
   if (warmup < 0) return set_error(PS_ERR_ARG, "warmup must be >= 0");
   int rc = validate_desc(desc);
@@ -1112,6 +1113,7 @@ int ps_run_host_batch_ex(ps_ctx* ctx, int n, const ps_kernel_desc* descs, const 
   if (!outputs && !checksums) return set_error(PS_ERR_ARG, "ps_run_host_batch: neither outputs nor checksums");
   *seconds = 0.0;
   if (n == 0) return PS_OK;
+  TraceRange trace("ps_run_host_batch (e2e)");
   PS_CUDA(cudaSetDevice(c->device));
   // Every kernel's arrays get a region of one device arena, placed as a ring
   // in batch order. The copy-in stream only waits where a region is reused
@@ -1273,3 +1275,13 @@ int ps_host_free(void* ptr) {
 }
 
 }  // extern "C"
+
+extern "C" int ps_trace_push(const char* name) {
+  nvtxRangePushA(name ? name : "");
+  return PS_OK;
+}
+
+extern "C" int ps_trace_pop(void) {
+  nvtxRangePop();
+  return PS_OK;
+}

@@ -10,9 +10,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../../include/perfseer_b200.h"
 
 namespace ps {
+
+// NVTX range over a host-side stage (header-only NVTX v3: free unless a
+// profiler is attached); shows ps_measure / fits / evaluations in nsys/ncu
+// timelines (SURVEY §5 tracing).
+struct TraceRange {
+  explicit TraceRange(const char* name) { nvtxRangePushA(name); }
+  ~TraceRange() { nvtxRangePop(); }
+  TraceRange(const TraceRange&) = delete;
+  TraceRange& operator=(const TraceRange&) = delete;
+};
 
 struct DevBuf {
   void* ptr = nullptr;

@@ -178,3 +178,18 @@ def geo_mean_rel_error(pred, meas) -> float:
     out = C.c_double()
     check(_declare().ps_geo_mean_rel_error(_dptr(p), _dptr(m), len(p), C.byref(out)))
     return out.value
+
+def trace(name: str):
+    """NVTX range over a pipeline stage (ps_trace_push/pop): `with trace("sweep"): ...`."""
+    import contextlib
+
+    @contextlib.contextmanager
+    def _range():
+        L = lib()
+        L.ps_trace_push.argtypes = [C.c_char_p]
+        L.ps_trace_push(name.encode())
+        try:
+            yield
+        finally:
+            L.ps_trace_pop()
+    return _range()
