@@ -78,3 +78,10 @@ def test_process_options_validate_their_values():
             host.set_option(key, "sometimes")
     with _pytest.raises(PsError):
         host.set_option("no_such_option", "on")
+
+
+def test_trace_ranges_nest_without_a_profiler():
+    from paper_1904_09538_b200.host import trace
+    with trace("outer"):
+        with trace("inner"):
+            pass
