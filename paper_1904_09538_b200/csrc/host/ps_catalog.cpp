@@ -780,10 +780,11 @@ std::vector<Generator> b200_generators() {
                      {"n", {"1024", "2048", "4096", "8192"}}},
                     make_matmul_sq_rm));
   // BASELINE.json config 0: grids 1024^2..8192^2 (multiples of lcm(14, 16)).
-  // The application sweep adds 1680, 3360 and 6272 between the four
-  // calibration sizes: the held-out VALIDATION sizes of model selection.
+  // The application sweep adds 1680, 2800, 3360, 5600 and 6272 between the
+  // four calibration sizes: the held-out VALIDATION sizes of model selection.
   const std::vector<std::string> fd_n{"1120", "2240", "4480", "8176"};
-  const std::vector<std::string> fd_app_n{"1120", "1680", "2240", "3360", "4480", "6272", "8176"};
+  const std::vector<std::string> fd_app_n{"1120", "1680", "2240", "2800", "3360",
+                                          "4480", "5600", "6272", "8176"};
   out.push_back(gen("finite_diff", {{"dtype", {"float32"}}, {"tile", {"16x16", "18x18"}}, {"n", fd_app_n}},
                     make_fd_stencil));
   out.push_back(gen("finite_diff_rm",

@@ -225,7 +225,7 @@ FD_STORES = [("p_g16s", G16S), ("p_fd16res", _tag("fd-16x16-res")),
 FD = Workload(
     name="fd",
     description=("BASELINE.json configs[0]: five-point FD stencil, 16x16 and 18x18 tiles, "
-                 "grids 1120^2..8176^2 (7 sizes), calibrated from the microbenchmark sweep (gmem 16x16 and "
+                 "grids 1120^2..8176^2 (9 sizes), calibrated from the microbenchmark sweep (gmem 16x16 and "
                  "18x18 patterns) plus the fd-* work-removed kernels (PAPER.md:2560-2670); "
                  "18x18 sub-group counts use the ceil(324/32) extension (SURVEY A1)"),
     calibration_tags=MICRO_TAGS + [["gmem_pattern_18"], ["finite_diff_rm"]],
@@ -238,8 +238,8 @@ FD = Workload(
             "ldst": ldst_model(FD_LOADS, FD_STORES, ONCHIP[:3], ONCHIP[3:]),
             "ldst_g": ldst_model(FD_LOADS, FD_STORES, ONCHIP[:3], ONCHIP[3:], group_pipe=True)},
     variant_keys=("tile",),
-    # the three sizes between the four calibration sizes (ps_catalog.cpp)
-    validation_sizes=("n=1680", "n=3360", "n=6272"),
+    # the five sizes between the four calibration sizes (ps_catalog.cpp)
+    validation_sizes=("n=1680", "n=2800", "n=3360", "n=5600", "n=6272"),
     size_keys=("n",),
     extra={"options": {"partial_subgroups": "round_up"}},
     c5_coords={"n": 1},

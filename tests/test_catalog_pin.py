@@ -38,7 +38,7 @@ def port_output() -> str:
 def test_port_equals_reference_on_the_bench_catalog(port_output):
     want = GOLDEN.read_text().splitlines()
     got = port_output.splitlines()
-    assert len(got) == len(want) == 332
+    assert len(got) == len(want) == 336
     for g, w in zip(got, want):
         assert g == w, f"{json.loads(w)['id']}: port differs from the reference"
 

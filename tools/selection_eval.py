@@ -70,7 +70,7 @@ def evaluate(wl, app, meas, cands, rule, metric):
         best = min(cands, key=key)
         asg = {v: best for v in variants}
     else:  # per-variant: rankings first, then worst variant error
-        short = {v: sorted(cands, key=lambda c: verr(c, v))[:4] for v in variants}
+        short = {v: sorted(cands, key=lambda c: verr(c, v))[:TOP] for v in variants}
         best = None
         for combo in itertools.product(*[short[v] for v in variants]):
             a = dict(zip(variants, combo))
@@ -88,6 +88,9 @@ def evaluate(wl, app, meas, cands, rule, metric):
             "all_err": {v[-6:]: round(geo([rel(p, t) for k, p, t in rows if variant[k] == v]), 3)
                         for v in variants},
             "rank": bench._rank(wl, rows)["ranking_correct_gap_ge_2pct"]}
+
+
+TOP = None
 
 
 def main():
