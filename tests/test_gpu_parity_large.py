@@ -102,6 +102,16 @@ def test_fd_8176(dev, tile, mode):
             _bitwise(g, w, f"{v} {mode}")
 
 
+@pytest.mark.parametrize("n", [1680, 2800, 3360, 5600, 6272])
+@pytest.mark.parametrize("tile", ["16x16", "18x18"])
+def test_fd_validation_sizes(dev, tile, n):
+    """The application-only FD sizes the bench measures for model selection."""
+    v = vid("finite_diff", dtype="float32", tile=tile, n=n)
+    d, io = desc_io(v)
+    ins = make_inputs(d, io, "uniform", seed=7)
+    _bitwise(dev.run(d, ins)[0], oracle_suite.run(d, io, ins)[0], v)
+
+
 @pytest.mark.parametrize("mode", ["seed17", "uniform"])
 @pytest.mark.parametrize("np_", [16, 32, 48, 64, 96, 128])
 @pytest.mark.parametrize("variant", ["noPF", "uPF", "dmPF", "dmPFtrans"])
