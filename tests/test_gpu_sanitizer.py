@@ -47,6 +47,33 @@ print("ok")
 '''
 
 
+K18_CHUNKED = r'''
+import sys; sys.path.insert(0, ".")
+import numpy as np
+from paper_1904_09538_b200 import host, workloads as W
+from paper_1904_09538_b200.device import CudaDevice
+from paper_1904_09538_b200.predict import PredictionTables, c5_points
+host.set_option("partial_subgroups", "round_up")
+variants = []
+for g, wl in enumerate((W.MATMUL, W.FD, W.DG)):
+    m = host.HostModel(wl.models["ldst"])
+    tag = {"matmul": ["matmul_sq", "n:1024"], "fd": ["finite_diff", "n:1120"],
+           "dg": ["dg_diff", "nelements:10000", "nunit_nodes:64"]}[wl.name]
+    for vid, _ in host.catalog(tag):
+        variants.append({"id": vid, "model": m.text, "params": [1e-12] * len(m.params),
+                         "group": g, "coords": wl.c5_coords})
+t = PredictionTables(variants)
+pts = c5_points(500_000)
+with CudaDevice(0) as dev:
+    pp, pred, arg, keep = t.pinned_buffers(len(pts))
+    pp[:] = pts
+    t.eval_gpu(dev, pp, out=(pred, arg))
+    pc, ac = t.eval_cpu(pts[-1000:], threads=4)
+    assert np.array_equal(np.asarray(pred)[-1000:].view(np.uint64), pc.view(np.uint64))
+print("ok")
+'''
+
+
 def _run(args, code=None, timeout=900):
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not installed")
@@ -78,4 +105,11 @@ def test_memcheck_e2e_arena():
     rc, out = _run(["--tool", "memcheck", "--error-exitcode", "9"],
                    "import sys, pytest; sys.exit(pytest.main(['-q', '-x', '-p', 'no:cacheprovider', "
                    "'tests/test_gpu_e2e.py']))")
+    assert rc == 0 and "ERROR SUMMARY: 0 errors" in out, out[-3000:]
+
+
+def test_memcheck_k18_specialised_chunked():
+    """The run-time compiled K18 kernels over the chunked three-stream
+    pipeline (500k points, several chunks) under memcheck."""
+    rc, out = _run(["--tool", "memcheck", "--error-exitcode", "9"], K18_CHUNKED)
     assert rc == 0 and "ERROR SUMMARY: 0 errors" in out, out[-3000:]
