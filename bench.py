@@ -1178,13 +1178,35 @@ def run_ours(args, dist: Dist) -> None:
     dist.barrier()
     e2e_time = e2e_full_time = 0.0
     e2e_bytes = 0.0
+    last_sums = None
     with trace("bench: e2e through host buffers"):
         for _ in range(args.steps):
             if e2e_set:
-                e2e_time += dev.run_host_batch(batch, b_in, None, checksums=True)[0]
+                dt, last_sums = dev.run_host_batch(batch, b_in, None, checksums=True)
+                e2e_time += dt
                 if full_outputs:
                     e2e_full_time += dev.run_host_batch(batch, b_in, b_out)
             e2e_bytes += sum(ios[i].bytes_global for i in e2e_set)
+    # the pipelined pass's per-kernel checksums at bench size against a
+    # single launch of the same kernel on the same host inputs (ps_run_verify,
+    # no arena, no overlap): checks the ring placement, the stream ordering
+    # and the checksum reduction at the sizes the bench times (kernel values
+    # themselves are pinned by the parity tests)
+    e2e_verified = [0, 0]
+    if e2e_set and last_sums is not None:
+        big = sorted(range(len(e2e_set)), key=lambda p_: -ios[e2e_set[p_]].bytes_global)[:6]
+        spread = list(range(0, len(e2e_set), max(1, len(e2e_set) // 6)))[:6]
+        for pos in sorted(set(big + spread)):
+            i = e2e_set[pos]
+            dt = np.float32 if ios[i].elem_bytes == 4 else np.float64
+            # ps_run_verify on views of the pinned inputs; pageable outputs
+            # (the pinned budget is spent on the inputs)
+            outs = dev.run(descs[i], [a.numpy(dt) for a in pinned[i][0]])
+            want = sum(int(np.sum(o.view(np.uint32), dtype=np.uint64)) for o in outs) % (1 << 64)
+            e2e_verified[0] += int(int(last_sums[pos]) == want)
+            e2e_verified[1] += 1
+            del outs
+    e2e_verified = [int(dist.sum(float(x))) for x in e2e_verified]
     e2e_time_max = dist.max(e2e_time)
     e2e_full_time_max = dist.max(e2e_full_time)
     d2h_full = d2h
@@ -1418,7 +1440,8 @@ def run_ours(args, dist: Dist) -> None:
                                  suite=suite_binding),
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_bytes_all / e2e_time_max / 1e9, 3) if e2e_time_max else None,
-                "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+                "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "checksums_verified": f"{e2e_verified[0]}/{e2e_verified[1]}"},
         # headline accuracy: the per-variant held-out choice where it was
         # made, else the single held-out model of the application
         "accuracy": {
