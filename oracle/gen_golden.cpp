@@ -161,6 +161,31 @@ int main() {
                                              {"keep", "res"}, {"n", n}});
     kernels.push_back(run_kernel_json(rr.id, rr.kernel, rr.bindings, "res"));
   }
+  // DG differentiation (the B200 catalog's dg_diff, ps_catalog.cpp
+  // make_dg_diff; the reference has no DG generator): every variant computes
+  // res[m,k,i] = sum_j diff_mat[m,i,j] u[k,j] (dmPFtrans: u and res with the
+  // element index last). The staged variants are not functional under
+  // run_reference, so all four are pinned to the untiled source kernel, as
+  // the matmul PF case above; seed-pattern inputs keep every sum exact.
+  for (const auto& [nel, np] : std::vector<std::pair<std::string, std::string>>{
+           {"32", "16"}, {"48", "32"}}) {
+    const std::map<std::string, long long> b{{"nel", std::stoll(nel)}, {"np", std::stoll(np)}};
+    for (const std::string v : {"noPF", "uPF", "dmPF", "dmPFtrans"}) {
+      const bool trans = v == "dmPFtrans";
+      Kernel src = make_kernel(
+          "{[m,k,i,j]: 0<=m<3 and 0<=k<nel and 0<=i,j<np}",
+          {trans ? "res[m,i,k] = sum(j, diff_mat[m,i,j]*u[j,k])"
+                 : "res[m,k,i] = sum(j, diff_mat[m,i,j]*u[k,j])"},
+          {{"diff_mat", Dtype::float32, {"3", "np", "np"}},
+           {"u", Dtype::float32, trans ? std::vector<std::string>{"np", "nel"}
+                                       : std::vector<std::string>{"nel", "np"}},
+           {"res", Dtype::float32, trans ? std::vector<std::string>{"3", "np", "nel"}
+                                         : std::vector<std::string>{"3", "nel", "np"}}});
+      const std::string id = "dg_diff__dtype-float32__nelements-" + nel +
+                             "__nmatrices-3__nunit_nodes-" + np + "__variant-" + v;
+      kernels.push_back(run_kernel_json(id, src, b, "res"));
+    }
+  }
   root["kernels"] = kernels;
 
   // ---- 2./3. counts and features over the whole built-in catalog ----------
