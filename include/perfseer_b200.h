@@ -293,7 +293,8 @@ int ps_eval_batched(ps_ctx* ctx, const ps_tables* tables, const int64_t* points,
  * and loads it ahead of the first evaluation (jit_seconds: the time this
  * call spent); ps_eval_jit_source returns the generated CUDA source;
  * ps_eval_jit_compile compiles it without a device (cubin size out). Same
- * bits as the interpreter and ps_eval_cpu. */
+ * bits as the interpreter and ps_eval_cpu. Table sets whose generated source
+ * exceeds 512 KB (~150 variants) keep the interpreter. */
 int ps_eval_prepare(ps_ctx* ctx, const ps_tables* tables, double* jit_seconds);
 int ps_eval_jit_source(const ps_tables* tables, char* out, size_t cap, size_t* needed);
 int ps_eval_jit_compile(const ps_tables* tables, size_t* cubin_bytes);

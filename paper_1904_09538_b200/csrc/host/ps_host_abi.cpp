@@ -414,7 +414,7 @@ static int jit_kernel_for(ps_ctx* ctx, const ps_tables* tables, void** kernel, d
     return PS_OK;
   }
   const int rc = ps::k18_jit_kernel(c, tables->flat(), kernel, seconds);
-  if (rc == PS_OK) tables->jit[c->device] = *kernel;
+  if (rc == PS_OK) tables->jit[c->device] = *kernel;  // null: too large, the interpreter
   return rc;
 }
 
