@@ -115,3 +115,31 @@ def test_jit_kernel_matches_interpreter_bitwise(dev):
         host.set_option("k18_jit", "on")
     np.testing.assert_array_equal(np.asarray(gj).view(np.uint64), np.asarray(gi).view(np.uint64))
     assert np.array_equal(np.asarray(aj), np.asarray(ai))
+
+
+def test_large_variant_space_keeps_the_interpreter(dev):
+    """A table set whose generated kernel source exceeds the JIT limit is
+    evaluated by the table interpreter (no compile), with the same bits as
+    the CPU tables."""
+    from paper_1904_09538_b200 import host, workloads as W
+    from paper_1904_09538_b200.predict import PredictionTables, c5_points
+    text = W.MATMUL.models["ldst_g"]
+    m = host.HostModel(text)
+    vids = [v for v, _ in host.catalog(["matmul_sq", "n:1024"])]
+    rng = np.random.default_rng(4)
+    variants = []
+    for k in range(240):
+        params = list(rng.uniform(1e-13, 1e-11, len(m.params)))
+        for i, c in enumerate(m.cost_params):
+            if not c:
+                params[i] = 20.0
+        variants.append({"id": vids[k % len(vids)], "model": text, "params": params,
+                         "group": k % 8, "coords": {"n": 0}})
+    t = PredictionTables(variants)
+    assert len(t.jit_source()) > (1 << 19)
+    assert t.prepare_gpu(dev) == 0.0
+    pts = c5_points(3000, seed=8)
+    pg, ag, _ = t.eval_gpu(dev, pts)
+    pc, ac = t.eval_cpu(pts, threads=4)
+    np.testing.assert_array_equal(np.asarray(pg).view(np.uint64), pc.view(np.uint64))
+    assert np.array_equal(np.asarray(ag), ac)
