@@ -36,6 +36,7 @@ def _worker(rank: int, world: int, port: int, q) -> None:
         table = dist.gather_table(records)
         load = sum(est[i] for i, _ in mine)
         mx = dist.max(load)
+        total = dist.sum(float(len(mine)))  # launch counts add over ranks
         dist.barrier()
         # C5 prediction sharding: contiguous point blocks per rank, predictions
         # and argmins all-gathered; the fitted variants come from rank 0
@@ -56,7 +57,7 @@ def _worker(rank: int, world: int, port: int, q) -> None:
         A = dist.all_gather_rows(a.astype(np.float64)).astype(np.int64)
         fp, fa = t.eval_cpu(pts)
         c5 = (hi - lo, bool(np.array_equal(P, fp)), bool(np.array_equal(A, fa.astype(np.int64))))
-        q.put((rank, len(mine), sorted(table), load, mx, len(units), c5))
+        q.put((rank, len(mine), sorted(table), load, mx, len(units), c5, total))
         dist.close()
     except Exception as e:  # surfaced by the parent
         q.put((rank, "error", repr(e)))
@@ -108,3 +109,9 @@ def test_c5_points_sharded_and_gathered(results):
     for r in (0, 1):
         assert results[r][6][1], "gathered predictions equal the single-rank evaluation"
         assert results[r][6][2], "gathered argmins equal the single-rank evaluation"
+
+
+def test_sum_over_ranks(results):
+    # every rank sees the whole job's unit count
+    n_units = results[0][5]
+    assert all(item[7] == n_units for item in results.values())
