@@ -657,14 +657,14 @@ int launch(Ctx* c, const ps_kernel_desc* d) {
                                                        (float*)out0, n);
         else
           matmul_nopf<float><<<grid, block, 0, st>>>((const float*)in0, (const float*)in1,
-                                                     (float*)out0, n, 16);
+                                                     (float*)out0, n, 16, kMatmulPanel);
       } else {
         if (d->prefetch)
           matmul_pf<double, 16><<<grid, block, 0, st>>>((const double*)in0, (const double*)in1,
                                                         (double*)out0, n);
         else
           matmul_nopf<double><<<grid, block, 0, st>>>((const double*)in0, (const double*)in1,
-                                                      (double*)out0, n, 16);
+                                                      (double*)out0, n, 16, kMatmulPanel);
       }
       break;
     }
@@ -674,14 +674,16 @@ int launch(Ctx* c, const ps_kernel_desc* d) {
 #define PS_MM_RM(T)                                                                      \
   if (d->prefetch) {                                                                     \
     if (d->keep == PS_KEEP_A)                                                            \
-      matmul_rm<T, true, 1><<<grid, block, 0, st>>>((const T*)in0, (T*)out0, n, 16);     \
+      matmul_rm<T, true, 1><<<grid, block, 0, st>>>((const T*)in0, (T*)out0, n, 16, 0);  \
     else                                                                                 \
-      matmul_rm<T, true, 2><<<grid, block, 0, st>>>((const T*)in0, (T*)out0, n, 16);     \
+      matmul_rm<T, true, 2><<<grid, block, 0, st>>>((const T*)in0, (T*)out0, n, 16, 0);  \
   } else {                                                                               \
     if (d->keep == PS_KEEP_A)                                                            \
-      matmul_rm<T, false, 1><<<grid, block, 0, st>>>((const T*)in0, (T*)out0, n, 16);    \
+      matmul_rm<T, false, 1><<<grid, block, 0, st>>>((const T*)in0, (T*)out0, n, 16,     \
+                                                      kMatmulPanel);                     \
     else                                                                                 \
-      matmul_rm<T, false, 2><<<grid, block, 0, st>>>((const T*)in0, (T*)out0, n, 16);    \
+      matmul_rm<T, false, 2><<<grid, block, 0, st>>>((const T*)in0, (T*)out0, n, 16,     \
+                                                      kMatmulPanel);                     \
   }
       if (d->dtype == PS_F32) {
         PS_MM_RM(float)

@@ -240,15 +240,40 @@ __global__ void __launch_bounds__(256) overlap_rows(const float* __restrict__ in
 }
 
 // ---------------------------------------------------------------------------
+// Work-group order of the 16x16 matmul grids (the IR fixes which work-items a
+// group holds, not the order the hardware runs groups in): with W > 0 the
+// square grid is walked row-major inside panels of W block columns. The CTAs
+// co-resident on an SM still share one block row (its a rows stay in L1), but
+// a wave's b working set shrinks from all of b to W block columns, which fits
+// L2 — at n = 8192 the default order streams b from DRAM ~220 times
+// (tools/exp/mm_panel.cu: noPF 161 -> 122 ms, the b-column work-removed
+// kernel 116 -> 73 ms at W = 64; PF unchanged).
+constexpr int kMatmulPanel = 64;
+__device__ __forceinline__ void matmul_group(int W, int& bx, int& by) {
+  const int nb = (int)gridDim.x;
+  if (W <= 0 || W >= nb) {
+    bx = blockIdx.x;
+    by = blockIdx.y;
+    return;
+  }
+  const int id = blockIdx.y * nb + blockIdx.x;
+  const int per = W * (int)gridDim.y, p = id / per, r = id % per;
+  const int w = min(W, nb - p * W);
+  by = r / w;
+  bx = p * W + r % w;
+}
+
 // K9 matmul_sq noPF (uipick.cpp:478-502): c[i,j] = sum_k a[i,k]*b[k,j] with
 // i = 16*i_out + i_in (g.1, l.1), j = 16*j_out + j_in (g.0, l.0); one madd
 // per k in ascending order, accumulator starting at 0.
 template <typename T>
 __global__ void __launch_bounds__(256) matmul_nopf(const T* __restrict__ a,
                                                    const T* __restrict__ b, T* __restrict__ c,
-                                                   int n, int tile) {
-  const int i = blockIdx.y * tile + threadIdx.y;
-  const int j = blockIdx.x * tile + threadIdx.x;
+                                                   int n, int tile, int panel) {
+  int bx, by;
+  matmul_group(panel, bx, by);
+  const int i = by * tile + threadIdx.y;
+  const int j = bx * tile + threadIdx.x;
   const T* arow = a + (int64_t)i * n;
   const T* bcol = b + j;
   T acc = T(0);
@@ -324,10 +349,12 @@ __global__ void __launch_bounds__(TS* TS) matmul_pf(const T* __restrict__ a,
 // = tgt_read with lid(0) fastest. keep: 1 = a, 2 = b.
 template <typename T, bool PF, int KEEP>
 __global__ void __launch_bounds__(256) matmul_rm(const T* __restrict__ src,
-                                                 T* __restrict__ dest, int n, int tile) {
+                                                 T* __restrict__ dest, int n, int tile, int panel) {
   const int ti = threadIdx.y, tj = threadIdx.x;
-  const int row = blockIdx.y * tile + ti;
-  const int col = blockIdx.x * tile + tj;
+  int bx, by;
+  matmul_group(panel, bx, by);  // the order of the application kernel it times
+  const int row = by * tile + ti;
+  const int col = bx * tile + tj;
   T acc = T(0);
   if constexpr (PF) {
     const int ntiles = n / tile;

@@ -143,7 +143,7 @@ int main(int argc, char** argv) {
     cudaMemcpy(r0.data(), c0, N * 4, cudaMemcpyDeviceToHost);
     int reps = n == 8192 ? 3 : 10;
     {
-      float tp0 = time([&] { matmul_nopf<float><<<grid, block>>>(a, b, c, n, 16); }, reps);
+      float tp0 = time([&] { matmul_nopf<float><<<grid, block>>>(a, b, c, n, 16, 0); }, reps);
       float tp1 = time([&] { matmul_pf<float, 16><<<grid, block>>>(a, b, c, n); }, reps);
       printf("n %d product noPF %.3f ms  PF %.3f ms\n", n, tp0, tp1);
       float g0 = time([&] { nopf_p<0><<<grid, block>>>(a, b, c, n, 16); }, reps);
