@@ -1033,8 +1033,8 @@ def run_reference_arm(args, dist: Dist) -> None:
 # (profiles/r01_ncu_summary.csv): the paper variants are L1/shared-pipe bound
 # by their access semantics, not FP32 bound.
 BINDING = {
-    7: "L1/TEX: 88% (noPF n=8192; b loads 64 B per warp per madd) / 95% (PF, LDS wavefronts); "
-       "FMA pipe 14%",
+    7: "L1/TEX: 97% (noPF n=8192, panel order; b loads 64 B per warp per madd) / 95% (PF, LDS "
+       "wavefronts); FMA pipe 14-16%",
     11: "L1/TEX 96-97% (noPF, dmPF, profiles/r01_ncu_summary_dg_skew.csv), 88-96% (uPF, "
         "dmPFtrans); FMA pipe 14-26%",
     9: "HBM 5.1 TB/s of 6.56 (dram read+write 483 MB vs 535 MB algorithmic)",
@@ -1292,7 +1292,7 @@ def run_ours(args, dist: Dist) -> None:
                   "unit": "TB/s", "frac": round(ob / avg / 1e12 / l1_peak, 4),
                   "operand_bytes_per_launch": ob,
                   "basis": "IR operand loads per madd (a and b, work-item granularity) x 4 B; "
-                           "ncu l1tex throughput 88% (noPF) / 95% (PF) agrees"}
+                           "ncu l1tex throughput 97% (noPF, panel order) / 95% (PF) agrees"}
         return {"kernel": kernels[k], "bound": "fp32", "achieved": round(achieved, 3),
                 "binding_roofline": l1,
                 "peak": round(fp32_peak_tf, 2), "unit": "TFLOP/s",
@@ -1302,10 +1302,11 @@ def run_ours(args, dist: Dist) -> None:
                                "(SURVEY 8(d) C2; no tensor cores in the paper variants)",
                 "algorithmic_flops_per_launch": ios[k].flops,
                 "share_of_step": round(share[k] / total_t, 4),
-                "traffic_note": ("matmul noPF: DRAM bytes above the 12 n^2 compulsory are b-column "
-                                 "re-streams from L2 misses at ~450 GB/s, not binding; group-M rasters "
-                                 "cut them 60 -> 8.9 GB but run 30-50% slower (L1 a-row sharing), "
-                                 "tools/exp/mm_raster.cu, DESIGN.md K9") if d.gen == 7 else None,
+                "traffic_note": ("matmul noPF: work-groups run in panels of 64 block columns "
+                                 "(a wave's b columns fit L2): 2.8 GB of DRAM per launch at "
+                                 "n = 8192 against 0.8 GB compulsory (12 n^2), 60 GB in row-major "
+                                 "order (profiles/r02_ncu_summary_mm_panel.csv, DESIGN.md K9)")
+                if d.gen == 7 else None,
                 "note": "16x16 CUDA-core tiles by construction (uipick.cpp:464-554); the paper "
                         "reports 8-20% of FP32 peak for these variants (PAPER.md:2155-2157)"}
 
