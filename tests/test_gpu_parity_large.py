@@ -68,6 +68,27 @@ def test_matmul_bench_sizes_sampled_rows(dev, n, pf, mode):
         _bitwise(got[r], oracle_suite.matmul_rows(d, ins, r, r + 1), f"n={n} {pf} {mode} row {r}")
 
 
+@pytest.mark.parametrize("n", [1600, 2064, 6144])
+def test_matmul_nopf_partial_panels(dev, n):
+    """Work-group grids that are not a whole number of 64-column panels (100
+    and 129 block columns) and the bench's 6144 (6 panels): every work-group
+    still computes its own 16x16 block (sampled rows in every 16-row band
+    position, both edges, full output of the b-column work-removed kernel)."""
+    d, io = desc_io(_mm(n, "False"))
+    ins = make_inputs(d, io, "seed17")
+    got = dev.run(d, ins)[0].reshape(n, n)
+    rng = np.random.default_rng(n)
+    rows = sorted(set(rng.choice(n, 24, replace=False).tolist()) | {0, 15, 16, n - 17, n - 1})
+    for r in rows:
+        _bitwise(got[r], oracle_suite.matmul_rows(d, ins, r, r + 1), f"n={n} row {r}")
+    d, io = desc_io(vid("matmul_sq_rm", dtype="float32", prefetch="False", keep="b", lsize_0=16,
+                        lsize_1=16, groups_fit="True", n=n))
+    ins = make_inputs(d, io, "seed17")
+    got = dev.run(d, ins)[0].reshape(n, n)
+    want = np.repeat(ins[0].astype(np.float64).reshape(n, n).sum(axis=0)[None, :], n, axis=0)
+    np.testing.assert_array_equal(got.astype(np.float64), want)
+
+
 @pytest.mark.parametrize("keep", ["a", "b"])
 @pytest.mark.parametrize("pf", ["True", "False"])
 def test_matmul_rm_4096(dev, pf, keep):
